@@ -1,0 +1,496 @@
+/*
+ * fsqr_oracle.c — plain, slow, obviously-correct fp64 CPU FS-QRPPA.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * It shares no code with the CUDA path (paper_2601_02826_b200/): no headers,
+ * no helpers, no constants.  Every loop is written from the paper:
+ *
+ *   E1  PQR objective            PAPER.md:L61-66  (x_i includes the intercept; lambda_0 = 0)
+ *   E4  weighted l1
+ *   E7  column split             PAPER.md:L177-180 (contiguous near-equal blocks)
+ *   E12 FS-QRPPA update
+ *   L259 eta_g > mu*Lambda_max(X_g^T X_g), power method
+ *   E14 beta prox
+ *   E15 z prox
+ *   L287 aggregation X beta = sum_g X_g beta_g
+ *   Alg. 1
+ *   Prop. 1 saddle point / KKT
+ *   L404 standardised design     (x~_ij = (x_ij - m_j)/s_j, sample sd with n-1)
+ *
+ * Readings where the paper is silent (DESIGN.md §2 lists them all): the
+ * stopping rule is the relative KKT residual R = max(R_p, R_beta, R_z)
+ * (SURVEY §8(c) #3); initialisation beta=0, z=y, theta=0; lambda_max is the
+ * exact null-model threshold with a balanced subgradient at the tie.
+ *
+ * Determinism: every output element is computed by exactly one thread with a
+ * fixed summation order, so results do not depend on OMP_NUM_THREADS.
+ * Scalars that combine many elements (norms, objective) are summed serially.
+ *
+ * Parity pins (tests/test_oracle_*.py): prox closed forms vs brute-force 1-D
+ * minimisation, SPEC worked values, products vs numpy on small slabs, power
+ * method vs numpy.linalg.eigvalsh, brute-force LP vertex enumeration and
+ * HiGHS on tiny inputs, the lambda_max textbook case, partition invariance,
+ * Prop. 1 certificate, geometric decay (Corollary 1).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct {
+  int32_t storage;      /* 0 = fp32 dense, 1 = uint8 {0,1,2}, 2 = 2-bit packed */
+  int32_t pad_;
+  int64_t n, p, ld;     /* ld: floats (fp32) or bytes (u8 / 2-bit) per stored column */
+  const void* data;     /* data column c holds model column j = c + 1 */
+  const double* mean;   /* [p] m_j, or NULL until orc_colstats ran */
+  const double* sd;     /* [p] s_j */
+} orc_design;
+
+typedef struct {
+  double tau, mu;
+  int32_t G, check;     /* check = 0: run exactly max_iter iterations, ignore the stop test */
+  const double* eta;    /* [G] */
+  const double* lam;    /* [p+1], lam[0] = 0 (intercept unpenalised) */
+  int64_t max_iter;
+  double tol;
+} orc_opts;
+
+/* ---------------------------------------------------------------- design */
+
+static double raw(const orc_design* X, int64_t c, int64_t i) {
+  if (X->storage == 0) return (double)((const float*)X->data)[c * X->ld + i];
+  const uint8_t* b = (const uint8_t*)X->data;
+  if (X->storage == 1) return (double)b[c * X->ld + i];
+  return (double)((b[c * X->ld + i / 4] >> (2 * (i % 4))) & 3);
+}
+
+/* x~_ij: standardised design entry, column 0 is the all-ones intercept (L404) */
+double orc_xt(const orc_design* X, int64_t j, int64_t i) {
+  if (j == 0) return 1.0;
+  return (raw(X, j - 1, i) - X->mean[j - 1]) / X->sd[j - 1];
+}
+
+/* sample mean and sample sd (n-1 divisor), two-pass; returns 0 or -(1+c) for a zero-variance column */
+int64_t orc_colstats(const orc_design* X, double* mean, double* sd) {
+  int64_t bad = -1;
+#pragma omp parallel for schedule(dynamic, 256) if (X->n * X->p > 200000)
+  for (int64_t c = 0; c < X->p; ++c) {
+    double s = 0.0;
+    for (int64_t i = 0; i < X->n; ++i) s += raw(X, c, i);
+    double m = s / (double)X->n;
+    double v = 0.0;
+    for (int64_t i = 0; i < X->n; ++i) { double d = raw(X, c, i) - m; v += d * d; }
+    mean[c] = m;
+    sd[c] = sqrt(v / (double)(X->n - 1));
+    if (!(sd[c] > 0.0)) {
+#pragma omp critical
+      if (bad < 0 || c < bad) bad = c;
+    }
+  }
+  return bad < 0 ? 0 : -(1 + bad);
+}
+
+/* contiguous near-equal partition of ncols columns into G blocks */
+void orc_blocks(int64_t ncols, int32_t G, int64_t* start) {
+  int64_t q = ncols / G, rem = ncols % G;
+  start[0] = 0;
+  for (int32_t g = 0; g < G; ++g) start[g + 1] = start[g] + q + (g < rem ? 1 : 0);
+}
+
+static int32_t block_of(int64_t j, const int64_t* start, int32_t G) {
+  int32_t g = 0;
+  while (g + 1 < G && j >= start[g + 1]) ++g;
+  return g;
+}
+
+/* ------------------------------------------------------------- products */
+
+/* g_j = sum_i x~_ij theta_i for model columns j in [j0, j1)  (X_g^T theta, E14 input) */
+void orc_backprod_range(const orc_design* X, const double* theta, int64_t j0, int64_t j1, double* g) {
+#pragma omp parallel for schedule(dynamic, 64) if (X->n * (j1 - j0) > 200000)
+  for (int64_t j = j0; j < j1; ++j) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < X->n; ++i) acc += orc_xt(X, j, i) * theta[i];
+    g[j - j0] = acc;
+  }
+}
+
+void orc_backprod(const orc_design* X, const double* theta, double* g) {
+  orc_backprod_range(X, theta, 0, X->p + 1, g);
+}
+
+/* s_i = sum_j x~_ij b_j over model columns j in [j0, j1), in ascending j for every i.
+ * Terms with b_j == 0 are exactly +0 and are skipped.  Threads own row ranges. */
+void orc_fwdprod_range(const orc_design* X, const double* b, int64_t j0, int64_t j1, double* s) {
+  const int64_t n = X->n;
+#pragma omp parallel if (n * (j1 - j0) > 200000)
+  {
+#ifdef _OPENMP
+    extern int omp_get_thread_num(void);
+    extern int omp_get_num_threads(void);
+    int64_t nt = omp_get_num_threads(), t = omp_get_thread_num();
+#else
+    int64_t nt = 1, t = 0;
+#endif
+    int64_t i0 = n * t / nt, i1 = n * (t + 1) / nt;
+    for (int64_t i = i0; i < i1; ++i) s[i] = 0.0;
+    for (int64_t j = j0; j < j1; ++j) {
+      double bj = b[j - j0];
+      if (bj == 0.0) continue;
+      for (int64_t i = i0; i < i1; ++i) s[i] += orc_xt(X, j, i) * bj;
+    }
+  }
+}
+
+void orc_fwdprod(const orc_design* X, const double* beta, double* s) {
+  orc_fwdprod_range(X, beta, 0, X->p + 1, s);
+}
+
+/* --------------------------------------------------------------- proxes */
+
+static double pos(double v) { return v > 0.0 ? v : 0.0; }
+
+/* E14: beta+ = (1/eta)[(eta*beta + g - lam)_+ - (-eta*beta - g - lam)_+] */
+double orc_prox_beta(double beta, double g, double lam, double eta) {
+  return (pos(eta * beta + g - lam) - pos(-eta * beta - g - lam)) / eta;
+}
+
+/* E15: z+ = (z + theta/mu - tau/(n mu))_+ - (-z - theta/mu - (1-tau)/(n mu))_+ */
+double orc_prox_z(double z, double theta, double mu, double tau, int64_t n) {
+  return pos(z + theta / mu - tau / ((double)n * mu)) - pos(-z - theta / mu - (1.0 - tau) / ((double)n * mu));
+}
+
+/* E12 dual step: theta+ = theta - mu/(G+1) * (2 r+ - r) */
+double orc_dual(double theta, double r_new, double r_old, double mu, int32_t G) {
+  return theta - mu / (double)(G + 1) * (2.0 * r_new - r_old);
+}
+
+/* soft-threshold S_c(v) = sign(v) max(|v| - c, 0) (KKT residual) */
+static double soft(double v, double c) {
+  return v > c ? v - c : (v < -c ? v + c : 0.0);
+}
+
+/* prox of rho_tau with unit weight: P_tau(v) (KKT residual) */
+static double prox_rho(double v, double tau) {
+  return v > tau ? v - tau : (v < tau - 1.0 ? v + 1.0 - tau : 0.0);
+}
+
+/* pinball loss rho_tau(u) = (tau - 1{u<0}) u (L66) */
+double orc_rho(double u, double tau) { return (tau - (u < 0.0 ? 1.0 : 0.0)) * u; }
+
+/* --------------------------------------------------------- diagnostics */
+
+/* relative KKT residuals R_p, R_beta, R_z at w = (beta, z, theta) given g = X~^T theta and s = X~ beta */
+static void kkt_parts(int64_t n, int64_t p1, const double* y, double tau, const double* lam, const double* beta,
+                      const double* z, const double* theta, const double* g, const double* s, double* R) {
+  double rp = 0, yy = 0, rb = 0, bb = 0, gg = 0, rz = 0, zz = 0, tt = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    double r = s[i] + z[i] - y[i];
+    rp += r * r;
+    yy += y[i] * y[i];
+    double nt = (double)n * theta[i];
+    double d = z[i] - prox_rho(z[i] + nt, tau);
+    rz += d * d;
+    zz += z[i] * z[i];
+    tt += nt * nt;
+  }
+  for (int64_t j = 0; j < p1; ++j) {
+    double d = beta[j] - soft(beta[j] + g[j], lam[j]);
+    rb += d * d;
+    bb += beta[j] * beta[j];
+    gg += g[j] * g[j];
+  }
+  R[0] = sqrt(rp) / (1.0 + sqrt(yy));
+  R[1] = sqrt(rb) / (1.0 + sqrt(bb) + sqrt(gg));
+  R[2] = sqrt(rz) / (1.0 + sqrt(zz) + sqrt(tt));
+}
+
+void orc_kkt_rel(const orc_design* X, const double* y, double tau, const double* lam, const double* beta,
+                 const double* z, const double* theta, double* R) {
+  int64_t n = X->n, p1 = X->p + 1;
+  double* g = (double*)malloc(sizeof(double) * p1);
+  double* s = (double*)malloc(sizeof(double) * n);
+  orc_backprod(X, theta, g);
+  orc_fwdprod(X, beta, s);
+  kkt_parts(n, p1, y, tau, lam, beta, z, theta, g, s, R);
+  free(g);
+  free(s);
+}
+
+/* E1 objective: (1/n) sum rho_tau(y - X~ beta) + sum_{j>=1} lam_j |beta_j| */
+double orc_objective(const orc_design* X, const double* y, double tau, const double* lam, const double* beta) {
+  int64_t n = X->n, p1 = X->p + 1;
+  double* s = (double*)malloc(sizeof(double) * n);
+  orc_fwdprod(X, beta, s);
+  double loss = 0.0, pen = 0.0;
+  for (int64_t i = 0; i < n; ++i) loss += orc_rho(y[i] - s[i], tau);
+  for (int64_t j = 1; j < p1; ++j) pen += lam[j] * fabs(beta[j]);
+  free(s);
+  return loss / (double)n + pen;
+}
+
+/* Prop. 1 certificate: max violations of
+ *   (a) z = y - X~ beta,  (b) g_j in lam_j d|beta_j|,  (c) n theta_i in d rho_tau(z_i).  out[0..2] */
+void orc_kkt_cert(const orc_design* X, const double* y, double tau, const double* lam, const double* beta,
+                  const double* z, const double* theta, double* out) {
+  int64_t n = X->n, p1 = X->p + 1;
+  double* g = (double*)malloc(sizeof(double) * p1);
+  double* s = (double*)malloc(sizeof(double) * n);
+  orc_backprod(X, theta, g);
+  orc_fwdprod(X, beta, s);
+  double va = 0, vb = 0, vc = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    double a = fabs(y[i] - s[i] - z[i]);
+    if (a > va) va = a;
+    double t = (double)n * theta[i], v;
+    if (z[i] > 0) v = fabs(t - tau);
+    else if (z[i] < 0) v = fabs(t - (tau - 1.0));
+    else v = t > tau ? t - tau : (t < tau - 1.0 ? tau - 1.0 - t : 0.0);
+    if (v > vc) vc = v;
+  }
+  for (int64_t j = 0; j < p1; ++j) {
+    double v;
+    if (beta[j] > 0) v = fabs(g[j] - lam[j]);
+    else if (beta[j] < 0) v = fabs(g[j] + lam[j]);
+    else v = pos(fabs(g[j]) - lam[j]);
+    if (v > vb) vb = v;
+  }
+  out[0] = va;
+  out[1] = vb;
+  out[2] = vc;
+  free(g);
+  free(s);
+}
+
+/* ------------------------------------------------------------ power method */
+
+static uint64_t orc_mix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+/* start vector entry for model column j: 2*U - 1, U = top 53 bits of mix(seed ^ mix(j)) */
+double orc_power_start(uint64_t seed, int64_t j) {
+  uint64_t h = orc_mix(seed ^ orc_mix((uint64_t)j));
+  return 2.0 * ((double)(h >> 11) * 0x1.0p-53) - 1.0;
+}
+
+/* Lambda_max(X~_g^T X~_g) for model columns [j0, j1) by the power method (L259):
+ * v <- w/||w||, w = X~_g^T (X~_g v); estimate = v^T w (Rayleigh quotient);
+ * stop when |est_k - est_{k-1}| <= tol * est_k or after maxit steps. */
+double orc_power(const orc_design* X, int64_t j0, int64_t j1, double tol, int64_t maxit, uint64_t seed,
+                 int64_t* iters) {
+  int64_t m = j1 - j0, n = X->n;
+  double* v = (double*)malloc(sizeof(double) * m);
+  double* w = (double*)malloc(sizeof(double) * m);
+  double* u = (double*)malloc(sizeof(double) * n);
+  double nv = 0.0;
+  for (int64_t a = 0; a < m; ++a) { v[a] = orc_power_start(seed, j0 + a); nv += v[a] * v[a]; }
+  nv = sqrt(nv);
+  for (int64_t a = 0; a < m; ++a) v[a] /= nv;
+  double est = 0.0, prev = 0.0;
+  int64_t k;
+  for (k = 1; k <= maxit; ++k) {
+    orc_fwdprod_range(X, v, j0, j1, u);
+    orc_backprod_range(X, u, j0, j1, w);
+    est = 0.0;
+    double nw = 0.0;
+    for (int64_t a = 0; a < m; ++a) { est += v[a] * w[a]; nw += w[a] * w[a]; }
+    nw = sqrt(nw);
+    if (k > 1 && fabs(est - prev) <= tol * est) break;
+    prev = est;
+    if (!(nw > 0.0)) break;
+    for (int64_t a = 0; a < m; ++a) v[a] = w[a] / nw;
+  }
+  if (iters) *iters = k > maxit ? maxit : k;
+  free(v);
+  free(w);
+  free(u);
+  return est;
+}
+
+/* ----------------------------------------------------------- lambda_max */
+
+static int cmp_double(const void* a, const void* b) {
+  double x = *(const double*)a, y = *(const double*)b;
+  return (x > y) - (x < y);
+}
+
+/* lambda_max(tau) = max_{j>=1} |sum_i x~_ij psi_i| / n, psi the null-model score with the
+ * intercept at the sample tau-quantile q = y_(ceil(n tau)); ties at q share the value that
+ * makes sum psi = 0, so psi is a valid subgradient and lambda >= lambda_max gives beta_{1..p} = 0. */
+double orc_lambda_max(const orc_design* X, const double* y, double tau, double* q_out) {
+  int64_t n = X->n, p1 = X->p + 1;
+  double* ys = (double*)malloc(sizeof(double) * n);
+  memcpy(ys, y, sizeof(double) * n);
+  qsort(ys, (size_t)n, sizeof(double), cmp_double);
+  int64_t k = (int64_t)ceil((double)n * tau);
+  if (k < 1) k = 1;
+  if (k > n) k = n;
+  double q = ys[k - 1];
+  free(ys);
+  int64_t nb = 0, ne = 0, na = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (y[i] < q) ++nb; else if (y[i] > q) ++na; else ++ne;
+  }
+  double tie = -((double)nb * (tau - 1.0) + (double)na * tau) / (double)ne;
+  double* psi = (double*)malloc(sizeof(double) * n);
+  for (int64_t i = 0; i < n; ++i) psi[i] = (y[i] < q ? tau - 1.0 : (y[i] > q ? tau : tie)) / (double)n;
+  double* g = (double*)malloc(sizeof(double) * p1);
+  orc_backprod(X, psi, g);
+  double lm = 0.0;
+  for (int64_t j = 1; j < p1; ++j) if (fabs(g[j]) > lm) lm = fabs(g[j]);
+  if (q_out) *q_out = q;
+  free(psi);
+  free(g);
+  return lm;
+}
+
+/* --------------------------------------------------------------- solver */
+
+/*
+ * Algorithm 1 from the state (beta, z, theta) given in-place.
+ * Iteration k:
+ *   g = X~^T theta^k;  R(w^k) from (beta^k, z^k, theta^k, g, s^k);
+ *   stop if check && R <= tol (status 0), or k == max_iter (status 2);
+ *   beta^{k+1}_j = E14(beta^k_j, g_j, lam_j, eta_{G(j)})     ParFor over blocks
+ *   z^{k+1}      = E15(z^k, theta^k)
+ *   s^{k+1}      = X~ beta^{k+1}                             (sum over blocks, L287)
+ *   r^{k+1}      = s^{k+1} + z^{k+1} - y
+ *   theta^{k+1}  = theta^k - mu/(G+1) (2 r^{k+1} - r^k)      E12
+ * trace (optional, [max_iter+1][5]): R_p, R_beta, R_z, objective(w^k), |support(beta^k)|.
+ * Returns 0 converged, 2 max_iter reached, -3 non-finite state.
+ */
+int orc_solve(const orc_design* X, const double* y, const orc_opts* o, double* beta, double* z, double* theta,
+              int64_t* iters, double* R, double* obj, double* trace) {
+  const int64_t n = X->n, p1 = X->p + 1;
+  int64_t* start = (int64_t*)malloc(sizeof(int64_t) * (o->G + 1));
+  orc_blocks(p1, o->G, start);
+  int32_t* blk = (int32_t*)malloc(sizeof(int32_t) * p1);
+  for (int64_t j = 0; j < p1; ++j) blk[j] = block_of(j, start, o->G);
+  double* g = (double*)malloc(sizeof(double) * p1);
+  double* s = (double*)malloc(sizeof(double) * n);
+  double* r = (double*)malloc(sizeof(double) * n);
+  orc_fwdprod(X, beta, s);
+  for (int64_t i = 0; i < n; ++i) r[i] = s[i] + z[i] - y[i];
+  const double sigma = o->mu / (double)(o->G + 1);
+  int status = 2;
+  int64_t k = 0;
+  for (;; ++k) {
+    orc_backprod(X, theta, g);
+    double Rk[3];
+    kkt_parts(n, p1, y, o->tau, o->lam, beta, z, theta, g, s, Rk);
+    double loss = 0.0, pen = 0.0;
+    int64_t nnz = 0;
+    for (int64_t i = 0; i < n; ++i) loss += orc_rho(y[i] - s[i], o->tau);
+    for (int64_t j = 1; j < p1; ++j) { pen += o->lam[j] * fabs(beta[j]); nnz += beta[j] != 0.0; }
+    double ob = loss / (double)n + pen;
+    if (trace) {
+      trace[5 * k + 0] = Rk[0];
+      trace[5 * k + 1] = Rk[1];
+      trace[5 * k + 2] = Rk[2];
+      trace[5 * k + 3] = ob;
+      trace[5 * k + 4] = (double)nnz;
+    }
+    if (R) { R[0] = Rk[0]; R[1] = Rk[1]; R[2] = Rk[2]; }
+    if (obj) *obj = ob;
+    if (!isfinite(Rk[0]) || !isfinite(Rk[1]) || !isfinite(Rk[2])) { status = -3; break; }
+    double Rmax = fmax(Rk[0], fmax(Rk[1], Rk[2]));
+    if (o->check && Rmax <= o->tol) { status = 0; break; }
+    if (k == o->max_iter) { status = 2; break; }
+    /* ParFor g: beta_g^{k+1} by E14 */
+    for (int64_t j = 0; j < p1; ++j) beta[j] = orc_prox_beta(beta[j], g[j], o->lam[j], o->eta[blk[j]]);
+    /* z^{k+1} by E15 (uses z^k, theta^k) */
+    for (int64_t i = 0; i < n; ++i) z[i] = orc_prox_z(z[i], theta[i], o->mu, o->tau, n);
+    /* theta^{k+1} by E12 */
+    orc_fwdprod(X, beta, s);
+    for (int64_t i = 0; i < n; ++i) {
+      double rn = s[i] + z[i] - y[i];
+      theta[i] = orc_dual(theta[i], rn, r[i], o->mu, o->G);
+      r[i] = rn;
+    }
+  }
+  (void)sigma;
+  if (iters) *iters = k;
+  free(start);
+  free(blk);
+  free(g);
+  free(s);
+  free(r);
+  return status;
+}
+
+/*
+ * Warm-started lambda path for one tau.
+ * lam_t = lam_path[t] * w_j (w_0 = 0).  The iterate w^k that first satisfies
+ * R(w^k) <= tol at lam_t (or reaches max_iter_point iterations at that point)
+ * is recorded as point t; the update of that same iteration k is still taken
+ * with lam_t, and iteration k+1 onward uses lam_{t+1} (the GPU state machine
+ * switches lambda between the check and the next X~^T theta pass).
+ * Outputs per point: iters[t] (iterations spent at the point), R_out[3t..],
+ * obj[t], beta_path[t*(p+1)..] (dense, optional).  Returns total iterations.
+ */
+int64_t orc_path(const orc_design* X, const double* y, double tau, double mu, int32_t G, const double* eta,
+                 const double* w, const double* lam_path, int32_t T, double tol, int64_t max_iter_point,
+                 double* beta, double* z, double* theta, int64_t* iters, double* R_out, double* obj,
+                 double* beta_path, int32_t* converged) {
+  const int64_t n = X->n, p1 = X->p + 1;
+  int64_t* start = (int64_t*)malloc(sizeof(int64_t) * (G + 1));
+  orc_blocks(p1, G, start);
+  int32_t* blk = (int32_t*)malloc(sizeof(int32_t) * p1);
+  for (int64_t j = 0; j < p1; ++j) blk[j] = block_of(j, start, G);
+  double* lam = (double*)malloc(sizeof(double) * p1);
+  double* g = (double*)malloc(sizeof(double) * p1);
+  double* s = (double*)malloc(sizeof(double) * n);
+  double* r = (double*)malloc(sizeof(double) * n);
+  orc_fwdprod(X, beta, s);
+  for (int64_t i = 0; i < n; ++i) r[i] = s[i] + z[i] - y[i];
+  int32_t t = 0;
+  for (int64_t j = 0; j < p1; ++j) lam[j] = lam_path[0] * w[j];
+  int64_t k = 0, kpt = 0;
+  for (;; ++k) {
+    orc_backprod(X, theta, g);
+    double Rk[3];
+    kkt_parts(n, p1, y, tau, lam, beta, z, theta, g, s, Rk);
+    double Rmax = fmax(Rk[0], fmax(Rk[1], Rk[2]));
+    int switch_now = 0;
+    if (Rmax <= tol || kpt == max_iter_point) {
+      double loss = 0.0, pen = 0.0;
+      for (int64_t i = 0; i < n; ++i) loss += orc_rho(y[i] - s[i], tau);
+      for (int64_t j = 1; j < p1; ++j) pen += lam[j] * fabs(beta[j]);
+      iters[t] = kpt;
+      R_out[3 * t] = Rk[0];
+      R_out[3 * t + 1] = Rk[1];
+      R_out[3 * t + 2] = Rk[2];
+      obj[t] = loss / (double)n + pen;
+      converged[t] = Rmax <= tol;
+      if (beta_path) memcpy(beta_path + (int64_t)t * p1, beta, sizeof(double) * p1);
+      if (t == T - 1) break;
+      switch_now = 1;
+    }
+    for (int64_t j = 0; j < p1; ++j) beta[j] = orc_prox_beta(beta[j], g[j], lam[j], eta[blk[j]]);
+    for (int64_t i = 0; i < n; ++i) z[i] = orc_prox_z(z[i], theta[i], mu, tau, n);
+    orc_fwdprod(X, beta, s);
+    for (int64_t i = 0; i < n; ++i) {
+      double rn = s[i] + z[i] - y[i];
+      theta[i] = orc_dual(theta[i], rn, r[i], mu, G);
+      r[i] = rn;
+    }
+    ++kpt;
+    if (switch_now) {
+      ++t;
+      kpt = 0;
+      for (int64_t j = 0; j < p1; ++j) lam[j] = lam_path[t] * w[j];
+    }
+  }
+  free(start);
+  free(blk);
+  free(lam);
+  free(g);
+  free(s);
+  free(r);
+  return k;
+}

@@ -1,0 +1,338 @@
+"""Pins for the oracle (CPU only): it is checked against what the paper and the mathematics
+fix, never against itself.  Each test names the passage it pins."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+from oracle import lp
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = json.load(open(os.path.join(HERE, "golden", "worked_values.json")))
+
+
+# ----------------------------------------------------------------- proxes (E14, E15, E12)
+
+@pytest.mark.parametrize("case", GOLD["prox_beta"])
+def test_prox_beta_worked_values(case):
+    v = oracle.prox_beta(case["beta"], case["g"], case["lam"], case["eta"])
+    assert v == pytest.approx(case["expect"], abs=1e-15), case["cite"]
+    if case["expect"] == 0.0:
+        assert v == 0.0  # exact zero in the dead zone
+
+
+@pytest.mark.parametrize("case", GOLD["prox_z"])
+def test_prox_z_worked_values(case):
+    v = oracle.prox_z(case["z"], case["theta"], case["mu"], case["tau"], case["n"])
+    assert v == pytest.approx(case["expect"], abs=1e-15), case["cite"]
+
+
+@pytest.mark.parametrize("case", GOLD["dual"])
+def test_dual_worked_values(case):
+    v = oracle.dual(case["theta"], case["r_new"], case["r_old"], case["mu"], case["G"])
+    assert v == pytest.approx(case["expect"], abs=1e-15), case["cite"]
+
+
+@pytest.mark.parametrize("case", GOLD["rho"])
+def test_rho_worked_values(case):
+    assert oracle.rho(case["u"], case["tau"]) == pytest.approx(case["expect"], abs=1e-15), case["cite"]
+
+
+def _argmin_1d(f, lo, hi):
+    """Brute force: dense grid then golden-section refinement (independent of the closed forms)."""
+    xs = np.linspace(lo, hi, 20001)
+    fx = np.array([f(x) for x in xs])
+    k = int(np.argmin(fx))
+    a, b = xs[max(k - 1, 0)], xs[min(k + 1, len(xs) - 1)]
+    gr = (np.sqrt(5) - 1) / 2
+    for _ in range(200):
+        c, d = b - gr * (b - a), a + gr * (b - a)
+        if f(c) < f(d):
+            b = d
+        else:
+            a = c
+    return 0.5 * (a + b)
+
+
+def test_prox_beta_bruteforce():
+    """E13/E14: beta+ = argmin lam|b| - g b + (eta/2)(b - beta)^2."""
+    rng = np.random.default_rng(1)
+    for _ in range(60):
+        beta, g = rng.normal(), rng.normal()
+        lam, eta = abs(rng.normal()) * rng.choice([0, 0.3, 1, 3]), rng.uniform(0.2, 5)
+        f = lambda b: lam * abs(b) - g * b + 0.5 * eta * (b - beta) ** 2
+        ref = _argmin_1d(f, -20, 20)
+        assert oracle.prox_beta(beta, g, lam, eta) == pytest.approx(ref, abs=1e-7)
+
+
+def test_prox_z_bruteforce():
+    """E15: z+ = argmin (1/n) rho_tau(z) - theta z + (mu/2)(z - z^k)^2."""
+    rng = np.random.default_rng(2)
+    for _ in range(60):
+        tau = rng.uniform(0.05, 0.95)
+        n = int(rng.integers(1, 50))
+        mu = rng.uniform(0.05, 3)
+        z0, th = rng.normal(), rng.normal() * 0.1
+        f = lambda z: (tau - (z < 0)) * z / n - th * z + 0.5 * mu * (z - z0) ** 2
+        ref = _argmin_1d(f, -20, 20)
+        assert oracle.prox_z(z0, th, mu, tau, n) == pytest.approx(ref, abs=1e-7)
+
+
+# ----------------------------------------------------------------- design + products
+
+def _np_standardized(prob):
+    """Independent numpy construction of X~ (n x (p+1)) from the stored bytes (L404)."""
+    if prob.storage == datagen.STORAGE_F32:
+        raw = prob.X[:, :prob.n].astype(np.float64).T
+    elif prob.storage == datagen.STORAGE_U8:
+        raw = prob.X[:, :prob.n].astype(np.float64).T
+    else:
+        b = prob.X.astype(np.int64)
+        codes = np.stack([(b >> (2 * q)) & 3 for q in range(4)], axis=2).reshape(prob.p, -1)
+        raw = codes[:, :prob.n].astype(np.float64).T
+    m = raw.mean(axis=0)
+    s = raw.std(axis=0, ddof=1)
+    return np.hstack([np.ones((prob.n, 1)), (raw - m) / s]), m, s
+
+
+@pytest.mark.parametrize("name,storage", [("c1", 0), ("c2", 1), ("c4", 2)])
+def test_colstats_and_products_vs_numpy(name, storage):
+    prob = datagen.make(name, n=37 if storage != 2 else 401, p=23, storage=storage)
+    d = oracle.Design.from_problem(prob)
+    A, m, s = _np_standardized(prob)
+    np.testing.assert_allclose(d.mean, m, rtol=1e-13, atol=1e-14)
+    np.testing.assert_allclose(d.sd, s, rtol=1e-13)
+    rng = np.random.default_rng(3)
+    th = rng.normal(size=prob.n)
+    be = rng.normal(size=prob.p + 1) * (rng.random(prob.p + 1) < 0.5)
+    np.testing.assert_allclose(oracle.backprod(d, th), A.T @ th, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(oracle.fwdprod(d, be), A @ be, rtol=1e-12, atol=1e-12)
+    # the standardised columns have mean 0 and sd 1
+    np.testing.assert_allclose(A[:, 1:].mean(axis=0), 0, atol=1e-12)
+    np.testing.assert_allclose(A[:, 1:].std(axis=0, ddof=1), 1, rtol=1e-12)
+
+
+def test_partition_invariance_products():
+    """X beta = sum_g X_g beta_g (L287) and X^T theta = concat_g X_g^T theta (E7)."""
+    prob = datagen.make("c2", n=64, p=101)
+    d = oracle.Design.from_problem(prob)
+    rng = np.random.default_rng(4)
+    th, be = rng.normal(size=prob.n), rng.normal(size=prob.p + 1)
+    full_s, full_g = oracle.fwdprod(d, be), oracle.backprod(d, th)
+    for G in (1, 2, 5, 10):
+        st = oracle.blocks(prob.p + 1, G)
+        s = sum(oracle.fwdprod(d, be[st[g]:st[g + 1]], st[g], st[g + 1]) for g in range(G))
+        gcat = np.concatenate([oracle.backprod(d, th, st[g], st[g + 1]) for g in range(G)])
+        np.testing.assert_allclose(s, full_s, rtol=1e-12, atol=1e-12)
+        np.testing.assert_array_equal(gcat, full_g)
+
+
+def test_blocks_split_rule():
+    """Contiguous near-equal blocks."""
+    assert list(np.diff(oracle.blocks(10, 3))) == [4, 3, 3]
+    assert list(np.diff(oracle.blocks(10, 1))) == [10]
+    sz = np.diff(oracle.blocks(2001, 5))
+    assert sz.sum() == 2001 and set(sz) <= {400, 401}
+
+
+def test_zero_variance_column_rejected():
+    X = np.zeros((3, 16), dtype=np.uint8)
+    X[0, :8] = [0, 1, 2, 0, 1, 2, 0, 1]
+    X[2, :8] = [1, 1, 0, 0, 1, 1, 0, 2]
+    with pytest.raises(ValueError, match="column 1"):
+        oracle.Design(1, 8, 3, 16, X)
+
+
+# ----------------------------------------------------------------- power method (L259)
+
+def test_power_vs_eigvalsh():
+    for seed, (n, p) in enumerate([(60, 9), (200, 50), (40, 39), (120, 7)]):
+        prob = datagen.make("c2", n=n, p=p, seed=100 + seed)
+        d = oracle.Design.from_problem(prob)
+        A, _, _ = _np_standardized(prob)
+        st = oracle.blocks(p + 1, 3)
+        for g in range(3):
+            B = A[:, st[g]:st[g + 1]]
+            ref = np.linalg.eigvalsh(B.T @ B)[-1]
+            est, _ = oracle.power(d, int(st[g]), int(st[g + 1]), tol=1e-12, maxit=100000)
+            assert est == pytest.approx(ref, rel=1e-6)
+
+
+def test_power_closed_forms():
+    """identity block -> 1; rank-one block u v^T -> ||u||^2 ||v||^2."""
+    n, p = 8, 5
+    X = np.zeros((p, 8), dtype=np.float32)
+    for c in range(p):
+        X[c, c] = 1.0
+    d = oracle.Design(0, n, p, 8, X, mean=np.zeros(p), sd=np.ones(p))
+    est, _ = oracle.power(d, 1, p + 1, tol=1e-14, maxit=1000)
+    assert est == pytest.approx(1.0, rel=1e-12)
+    u = np.array([1, 2, 0, -1, 3, 0, 1, 1], dtype=np.float64)
+    v = np.array([0.5, -1, 2, 1, 0.25])
+    X = np.outer(v, u).astype(np.float32)
+    d = oracle.Design(0, n, p, 8, X, mean=np.zeros(p), sd=np.ones(p))
+    est, _ = oracle.power(d, 1, p + 1, tol=1e-14, maxit=1000)
+    uu = X[0].astype(np.float64) / v[0]
+    assert est == pytest.approx(np.dot(uu, uu) * np.dot(v, v), rel=1e-6)
+
+
+# ----------------------------------------------------------------- solver pins
+
+def _tiny(seed, n=12, p=3, tau=0.5):
+    prob = datagen.make("c2", n=n, p=p, seed=seed)
+    d = oracle.Design.from_problem(prob)
+    return prob, d
+
+
+@pytest.mark.parametrize("seed,tau,lfrac", [(11, 0.5, 0.3), (12, 0.3, 0.1), (13, 0.7, 0.6), (14, 0.5, 0.0),
+                                            (15, 0.2, 0.05)])
+def test_solver_matches_lp_bruteforce(seed, tau, lfrac):
+    """FS-QRPPA converged objective == exact PQR optimum by vertex enumeration; HiGHS agrees."""
+    prob, d = _tiny(seed, tau=tau)
+    A, _, _ = _np_standardized(prob)
+    lm, _ = oracle.lambda_max(d, prob.y, tau)
+    lam = oracle.lam_vector(prob.p, lfrac * lm)
+    G, mu = 2, 0.1
+    eta = oracle.eta(d, G, mu)
+    out = oracle.solve(d, prob.y, tau, lam, eta, mu, G, max_iter=400000, tol=1e-11)
+    assert out["status"] == 0
+    fstar, _ = lp.vertex_enumeration(A, prob.y, tau, lam)
+    fh, _ = lp.highs(A, prob.y, tau, lam)
+    assert fh == pytest.approx(fstar, rel=1e-9, abs=1e-12)
+    assert out["obj"] == pytest.approx(fstar, rel=1e-8, abs=1e-12)
+    assert lp.pqr_objective(A, prob.y, tau, lam, out["beta"]) == pytest.approx(fstar, rel=1e-8, abs=1e-12)
+
+
+def test_kkt_certificate_and_fixed_point():
+    """Prop. 1: the converged state is a saddle point; a KKT point is a fixed point of one iteration."""
+    prob = datagen.make("c2", n=40, p=60, seed=21)
+    d = oracle.Design.from_problem(prob)
+    tau = 0.3
+    lm, _ = oracle.lambda_max(d, prob.y, tau)
+    lam = oracle.lam_vector(prob.p, 0.2 * lm)
+    G, mu = 5, 0.01
+    eta = oracle.eta(d, G, mu)
+    out = oracle.solve(d, prob.y, tau, lam, eta, mu, G, max_iter=400000, tol=1e-10)
+    assert out["status"] == 0
+    cert = oracle.kkt_cert(d, prob.y, tau, lam, out["beta"], out["z"], out["theta"])
+    assert cert.max() < 1e-6
+    st = (out["beta"], out["z"], out["theta"])
+    one = oracle.solve(d, prob.y, tau, lam, eta, mu, G, max_iter=1, check=False, state=st)
+    for a, b in zip(st, (one["beta"], one["z"], one["theta"])):
+        assert np.max(np.abs(a - b)) < 1e-8
+
+
+def test_lambda_max_null_model():
+    """At lambda >= lambda_max the solution is beta_{1..p} = 0 with intercept = the sample
+    tau-quantile (textbook); just below it, some beta_j != 0."""
+    prob = datagen.make("c2", n=101, p=40, seed=31)
+    d = oracle.Design.from_problem(prob)
+    G, mu = 4, 0.02
+    eta = oracle.eta(d, G, mu)
+    for tau in (0.5, 0.25):
+        lm, q = oracle.lambda_max(d, prob.y, tau)
+        assert q == np.sort(prob.y)[int(np.ceil(101 * tau)) - 1]
+        out = oracle.solve(d, prob.y, tau, oracle.lam_vector(prob.p, 1.01 * lm), eta, mu, G,
+                           max_iter=300000, tol=1e-10)
+        assert out["status"] == 0
+        assert np.all(out["beta"][1:] == 0.0)
+        assert out["beta"][0] == pytest.approx(q, abs=1e-6)
+        u = prob.y - q
+        assert out["obj"] == pytest.approx(np.mean(np.where(u < 0, (tau - 1) * u, tau * u)), rel=1e-7)
+        if tau == 0.5:  # mean |y - median| / 2
+            assert out["obj"] == pytest.approx(np.mean(np.abs(prob.y - np.median(prob.y))) / 2, rel=1e-7)
+        out = oracle.solve(d, prob.y, tau, oracle.lam_vector(prob.p, 0.9 * lm), eta, mu, G,
+                           max_iter=300000, tol=1e-10)
+        assert np.count_nonzero(out["beta"][1:]) >= 1
+
+
+def test_partition_invariance_solution():
+    """Theorem 1: the limit is a saddle point for every G."""
+    prob = datagen.make("c2", n=50, p=70, seed=41)
+    d = oracle.Design.from_problem(prob)
+    tau = 0.5
+    lm, _ = oracle.lambda_max(d, prob.y, tau)
+    lam = oracle.lam_vector(prob.p, 0.3 * lm)
+    objs, preds = [], []
+    for G in (1, 2, 5, 10):
+        mu = 0.03
+        eta = oracle.eta(d, G, mu)
+        out = oracle.solve(d, prob.y, tau, lam, eta, mu, G, max_iter=400000, tol=1e-9)
+        assert out["status"] == 0
+        objs.append(out["obj"])
+        preds.append(oracle.fwdprod(d, out["beta"]))
+    for o, s in zip(objs[1:], preds[1:]):
+        assert o == pytest.approx(objs[0], rel=1e-6)
+        np.testing.assert_allclose(s, preds[0], atol=1e-5)
+
+
+def test_geometric_decay():
+    """Corollary 1: dist(w^k, w_final) is dominated by a geometric sequence;
+    over the last 50 pre-stop iterations the log-distance slope is negative and the median
+    successive ratio <= 0.999."""
+    prob = datagen.make("c2", n=50, p=60, seed=51)
+    d = oracle.Design.from_problem(prob)
+    tau = 0.5
+    lm, _ = oracle.lambda_max(d, prob.y, tau)
+    lam = oracle.lam_vector(prob.p, 0.3 * lm)
+    G, mu = 3, 0.05
+    eta = oracle.eta(d, G, mu)
+    fin = oracle.solve(d, prob.y, tau, lam, eta, mu, G, max_iter=400000, tol=1e-12)
+    assert fin["status"] == 0
+    K = fin["iters"]
+    k0 = max(K - 60, 0)
+    w_fin = np.concatenate([fin["beta"], fin["z"], fin["theta"]])
+    base = oracle.solve(d, prob.y, tau, lam, eta, mu, G, max_iter=k0, check=False)
+    st = (base["beta"], base["z"], base["theta"])
+    dists = []
+    for _ in range(50):
+        dists.append(np.linalg.norm(np.concatenate(st) - w_fin))
+        o = oracle.solve(d, prob.y, tau, lam, eta, mu, G, max_iter=1, check=False, state=st)
+        st = (o["beta"], o["z"], o["theta"])
+    dd = np.array(dists[-50:])
+    dd = dd[dd > 0]
+    slope = np.polyfit(np.arange(len(dd)), np.log(dd), 1)[0]
+    assert slope < 0
+    assert np.median(dd[1:] / dd[:-1]) <= 0.999
+
+
+def test_thread_count_determinism():
+    """Fixed per-element summation order: bitwise-identical results for 1 and 4 threads."""
+    code = (
+        "import datagen, oracle, numpy as np;"
+        "pr=datagen.make('c2', n=70, p=130, seed=61); d=oracle.Design.from_problem(pr);"
+        "lm,_=oracle.lambda_max(d, pr.y, 0.5); lam=oracle.lam_vector(pr.p, 0.2*lm);"
+        "eta=oracle.eta(d, 3, 0.05);"
+        "o=oracle.solve(d, pr.y, 0.5, lam, eta, 0.05, 3, max_iter=300, check=False);"
+        "print(np.concatenate([o['beta'],o['z'],o['theta'],eta]).tobytes().hex())"
+    )
+    root = os.path.dirname(HERE)
+    outs = []
+    for t in ("1", "4"):
+        env = dict(os.environ, OMP_NUM_THREADS=t, PYTHONPATH=root)
+        outs.append(subprocess.check_output([sys.executable, "-c", code], env=env, cwd=root).strip())
+    assert outs[0] == outs[1]
+
+
+def test_path_warm_start_semantics():
+    """Warm-started path (L412): point t equals a cold solve at lam_t in objective (convex problem),
+    and the path's lambda_max end point is the null model."""
+    prob = datagen.make("c2", n=60, p=80, seed=71)
+    d = oracle.Design.from_problem(prob)
+    tau, G, mu = 0.5, 3, 0.03
+    eta = oracle.eta(d, G, mu)
+    lm, q = oracle.lambda_max(d, prob.y, tau)
+    lam_path = lm * 1.01 * (0.5 ** (np.arange(4) / 3))
+    res = oracle.path(d, prob.y, tau, lam_path, eta, mu, G, tol=1e-9, max_iter_point=300000)
+    assert res["converged"].all()
+    assert np.all(res["beta_path"][0, 1:] == 0)
+    for t in range(4):
+        cold = oracle.solve(d, prob.y, tau, oracle.lam_vector(prob.p, lam_path[t]), eta, mu, G,
+                            max_iter=300000, tol=1e-9)
+        assert cold["status"] == 0
+        assert res["obj"][t] == pytest.approx(cold["obj"], rel=1e-6)
