@@ -1,0 +1,207 @@
+/*
+ * fsqr.h — C ABI of the B200-native FS-QRPPA hot path (libfsqr.so).
+ *
+ * FS-QRPPA (§4, Algorithm 1) solves the l1-penalised
+ * quantile regression (PQR)
+ *
+ *     min_beta  (1/n) sum_i rho_tau(y_i - x~_i^T beta) + sum_{j>=1} lam_j |beta_j|      (E1, L61-66)
+ *
+ * on a column-split design X~ = [X~_1 | ... | X~_G] (E7, L177-180) with the
+ * Jacobi prox step on every beta_g (E14, L274-277) and on z (E15, L279-285)
+ * followed by the extrapolated dual step (E12, L247-257):
+ *
+ *     beta_g^{k+1} = (1/eta_g)[(eta_g beta_g^k + X~_g^T theta^k - lam_g)_+ - (-eta_g beta_g^k - X~_g^T theta^k - lam_g)_+]
+ *     z^{k+1}      = (z^k + theta^k/mu - tau/(n mu))_+ - (-z^k - theta^k/mu - (1-tau)/(n mu))_+
+ *     theta^{k+1}  = theta^k - mu/(G+1) [2 r^{k+1} - r^k],   r = X~ beta + z - y
+ *
+ * X~ is the standardised design: column 0 is a virtual
+ * all-ones intercept (lam_0 = 0, L155); model column j >= 1 is stored data
+ * column c = j-1 and standardised on the fly, x~_ij = (x_ij - m_j)/s_j with the
+ * sample mean m_j and sample sd s_j (n-1 divisor).
+ *
+ * Conventions
+ *  - Every pointer named *_dev is a device pointer; *_host is host memory.
+ *  - n-vectors for RHS r are stored contiguously: v[r*n + i].
+ *  - beta is stored coefficient-major: beta[j*n_rhs + r], j = 0..p.
+ *  - Streams: `stream` is a cudaStream_t (CUstream) handle passed as void*;
+ *    NULL means the legacy default stream.  All work is enqueued on it.
+ *  - No call aborts or prints.  Failures return a status < 0 and the message
+ *    is available from fsqr_last_error(ctx) (or fsqr_global_error() when no
+ *    context exists).  FSQR_NOT_CONVERGED is a flag, not an error: the state
+ *    is valid and readable.
+ *  - A context is single-writer and not thread-safe; distinct contexts are
+ *    independent.  Identical inputs give bitwise-identical outputs run to run.
+ *  - There is no CPU fallback: every step of the iteration runs in CUDA
+ *    kernels compiled for sm_100a.  A missing or non-sm_100 device is
+ *    FSQR_ERR_CUDA.
+ */
+#ifndef FSQR_H_
+#define FSQR_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FSQR_OK = 0,
+  FSQR_NOT_CONVERGED = 2,   /* max_iter reached; state valid */
+  FSQR_ERR_CONFIG = -1,     /* G < 1 or G > p+1, tau not in (0,1), mu <= 0, lambda < 0, bad storage/ld/sizes */
+  FSQR_ERR_DATA = -2,       /* zero-variance column (message names it), non-finite y */
+  FSQR_ERR_NUMERIC = -3,    /* NaN/Inf appeared in the state */
+  FSQR_ERR_CUDA = -4,       /* CUDA runtime/driver failure (message has the CUDA error string) */
+  FSQR_ERR_OOM = -5,        /* device allocation failed */
+  FSQR_ERR_STATE = -6       /* call not valid in the current state (e.g. path not run) */
+} fsqr_status;
+
+typedef enum {
+  FSQR_F32_DENSE = 0,   /* fp32, column-major, ld >= n floats, ld % 4 == 0 */
+  FSQR_U8 = 1,          /* genotype codes {0,1,2} one byte each, ld >= n bytes, ld % 16 == 0 */
+  FSQR_PACKED2 = 2      /* 2-bit codes, sample i at bits 2*(i%4) of byte i/4, ld >= ceil(n/4), ld % 16 == 0 */
+} fsqr_storage;
+
+typedef enum {
+  FSQR_BACKEND_AUTO = 0,    /* tcgen05 for U8 (if supported shape), else SIMT */
+  FSQR_BACKEND_TC = 1,      /* tcgen05.mma kind::i8, TMA-staged tiles (U8 only) */
+  FSQR_BACKEND_SIMT = 2     /* CUDA-core path (dp4a exact integer for U8/PACKED2, fp64 for F32) */
+} fsqr_backend;
+
+typedef struct {
+  int32_t storage;          /* fsqr_storage */
+  int32_t reserved;
+  int64_t n;                /* observations, 2 <= n <= 65536 */
+  int64_t p;                /* stored columns (the intercept is virtual and not stored) */
+  const void* data_dev;     /* BORROWED: [p][ld] column-major; must stay alive and unmodified for the ctx lifetime */
+  int64_t ld;               /* column stride in elements (F32) or bytes (U8, PACKED2); padding must be zero */
+  const double* mean_dev;   /* optional [p] m_j (NULL: computed, a0) */
+  const double* scale_dev;  /* optional [p] s_j (NULL: computed, a0); both or neither */
+} fsqr_design;
+
+typedef struct {
+  int32_t G;                /* number of column blocks (Remark 1, L307-310) */
+  int32_t backend;          /* fsqr_backend */
+  double mu;                /* augmented parameter mu > 0 (L259) */
+  double eta_safety;        /* eta_g = eta_safety * mu * Lambda_hat_g, default 1.05 */
+  const double* eta_host;   /* optional [G]: use these eta_g instead of the power method */
+  double tol;               /* stop when R(w^k) = max(R_p, R_beta, R_z) <= tol (reading R1) */
+  int64_t max_iter;         /* iteration cap for fsqr_solve */
+  int32_t power_max_iter;   /* power method cap (default 1000) */
+  int32_t trace_cap;        /* rows of the per-iteration trace ring buffer (default 4096) */
+  double power_tol;         /* power method relative tolerance (default 1e-4) */
+  uint64_t seed;            /* power-method start vector seed */
+  int64_t max_iter_point;   /* per-lambda-point cap in fsqr_path (default 10000) */
+} fsqr_options;
+
+typedef struct {
+  int64_t iterations;       /* outer iterations performed by this call */
+  int64_t total_iterations; /* iterations since create / set_state */
+  int32_t n_rhs;
+  int32_t status[16];       /* per RHS: 0 converged, 2 not converged, -3 numeric */
+  double R[16][3];          /* per RHS: R_p, R_beta, R_z at the committed iterate */
+  double objective[16];     /* per RHS: E1 at the committed iterate (standardised scale) */
+  double wall_ms;           /* device time of the call (CUDA events) */
+} fsqr_result;
+
+typedef struct fsqr_ctx fsqr_ctx;
+
+/* Fills defaults: G=5, backend AUTO, mu=0 (=> 2/n, reading R2), eta_safety 1.05, tol 1e-6,
+ * max_iter 100000, power 1000 / 1e-4, trace 4096, seed 0x5EED, max_iter_point 10000. */
+void fsqr_default_options(fsqr_options* opt);
+
+/*
+ * Create a solver for n_rhs (1..16) independent quantile levels sharing X.
+ * y_dev: [n] response (copied).  tau_host, lambda_host: [n_rhs] (copied);
+ * lambda_w_dev: optional [p+1] non-negative penalty weights w_j (lam_j = lambda * w_j,
+ * w_0 is ignored: the intercept is never penalised), NULL = all ones.
+ * Performs a0 (column statistics, exact integer sums for genotype storage),
+ * a0' (eta_g by the power method unless opt->eta_host) and lambda_max (per tau);
+ * cold start beta = 0, z = y, theta = 0.  Synchronises `stream`.
+ */
+fsqr_status fsqr_create(const fsqr_design* X, const double* y_dev, int32_t n_rhs, const double* tau_host,
+                        const double* lambda_host, const double* lambda_w_dev, const fsqr_options* opt,
+                        void* stream, fsqr_ctx** out);
+
+/* Enqueue exactly k outer iterations (a1-a5), ignoring the stopping test.  Asynchronous. */
+fsqr_status fsqr_iterate(fsqr_ctx* ctx, int64_t k, void* stream);
+
+/* Iterate until every RHS satisfies R(w^k) <= tol or max_iter total iterations (blocking).
+ * The committed iterate is the first w^k that passed (or the last one).  out may be NULL. */
+fsqr_status fsqr_solve(fsqr_ctx* ctx, fsqr_result* out, void* stream);
+
+/* E1 at the committed beta per RHS: (1/n) sum rho_tau(y - X~beta) + sum_{j>=1} lam_j |beta_j|
+ * (standardised scale).  Uses the cached s = X~beta (no pass over X).  Blocking. */
+fsqr_status fsqr_objective(fsqr_ctx* ctx, double* obj_host, void* stream);
+
+/* Relative KKT residuals [n_rhs][3] = (R_p, R_beta, R_z) at the committed iterate; one pass over X. Blocking. */
+fsqr_status fsqr_kkt(fsqr_ctx* ctx, double* R_host, void* stream);
+
+/* beta of the committed iterate, [n_rhs][p+1] row per RHS.
+ * scale 0: standardised; scale 1: original scale, beta_j/s_j and beta_0 - sum m_j beta_j/s_j (L404). */
+fsqr_status fsqr_get_beta(fsqr_ctx* ctx, double* beta_host, int32_t scale, void* stream);
+
+/* committed state: beta [n_rhs][p+1] (standardised), z [n_rhs][n], theta [n_rhs][n]; any may be NULL. */
+fsqr_status fsqr_get_state(fsqr_ctx* ctx, double* beta_host, double* z_host, double* theta_host, void* stream);
+
+/* warm start (Algorithm 1 inputs beta^0, z^0, theta^0, L290-292); layouts as fsqr_get_state; resets iteration counters. */
+fsqr_status fsqr_set_state(fsqr_ctx* ctx, const double* beta_host, const double* z_host, const double* theta_host,
+                           void* stream);
+
+/* change the penalty level per RHS (lambda_host [n_rhs]); the state is kept (warm start). */
+fsqr_status fsqr_set_lambda(fsqr_ctx* ctx, const double* lambda_host);
+
+/* lambda_max(tau) per RHS (null-model threshold, reading R4), computed on the GPU at create. */
+fsqr_status fsqr_lambda_max(const fsqr_ctx* ctx, double* out_host);
+
+/* eta_g [G] in use; column statistics m_j, s_j [p] (either may be NULL). */
+fsqr_status fsqr_get_eta(const fsqr_ctx* ctx, double* eta_host);
+fsqr_status fsqr_get_colstats(fsqr_ctx* ctx, double* mean_host, double* sd_host);
+
+/*
+ * Warm-started lambda path: RHS r walks lam_path_host[r*T + t],
+ * t = 0..T-1, all RHS in lockstep through one pass over X per iteration.  When R(w^k) <= tol at
+ * point t (or max_iter_point iterations were spent there) w^k is recorded as point t and RHS r moves
+ * to lam_{t+1} from the next iteration; after its last point it is frozen.  Blocking.
+ * iters_host [n_rhs][T], obj_host [n_rhs][T], R_host [n_rhs][T][3], nnz_host [n_rhs][T],
+ * converged_host [n_rhs][T] (any may be NULL).  Returns the lockstep iteration count in *total.
+ */
+fsqr_status fsqr_path(fsqr_ctx* ctx, const double* lam_path_host, int32_t T, int64_t* total, int64_t* iters_host,
+                      double* obj_host, double* R_host, int64_t* nnz_host, int32_t* converged_host, void* stream);
+
+/* Sparse solution of path point t for RHS r: writes up to cap (index j, beta_j standardised) pairs,
+ * returns the count in *count (which may exceed cap: then only cap were written). */
+fsqr_status fsqr_path_beta(fsqr_ctx* ctx, int32_t r, int32_t t, int64_t cap, int64_t* idx_host, double* beta_host,
+                           int64_t* count);
+
+/* Per-iteration trace [min(k, trace_cap)][n_rhs][5] = (R_p, R_beta, R_z, objective, |support|) of w^k
+ * for the last iterations, oldest first; returns rows written in *rows. */
+fsqr_status fsqr_trace(fsqr_ctx* ctx, double* out_host, int64_t cap_rows, int64_t* rows);
+
+/* total outer iterations since create/set_state (device counter; synchronises). */
+int64_t fsqr_iterations(fsqr_ctx* ctx);
+
+/* which X^T theta kernel is in use: "tc" or "simt" */
+const char* fsqr_backend_name(const fsqr_ctx* ctx);
+
+/*
+ * End-to-end convenience entry with HOST buffers (for users without device memory):
+ * copies X and y to the device on `stream`, creates a context, runs `iters` iterations
+ * (iters < 0: fsqr_solve), copies beta (standardised, [n_rhs][p+1]) back, destroys the
+ * context and frees the copies.  X->data_dev here points to HOST memory (pinned for speed).
+ */
+fsqr_status fsqr_fit_host(const fsqr_design* X_host, const double* y_host, int32_t n_rhs, const double* tau_host,
+                          const double* lambda_host, const fsqr_options* opt, int64_t iters, double* beta_host,
+                          fsqr_result* out, void* stream);
+
+const char* fsqr_last_error(const fsqr_ctx* ctx);
+const char* fsqr_global_error(void);
+const char* fsqr_status_str(fsqr_status s);
+
+/* frees everything the ctx owns (never the borrowed X). NULL is a no-op. */
+void fsqr_destroy(fsqr_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FSQR_H_ */

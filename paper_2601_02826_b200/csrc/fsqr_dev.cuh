@@ -1,0 +1,339 @@
+// fsqr_dev.cuh — device-side state, PTX wrappers and the shared epilogue of the
+// FS-QRPPA hot path (sm_100a).  Shared by every kernel translation unit.
+//
+// Arithmetic design:
+//  * a1 (X~^T theta) is computed EXACTLY in integers for genotype storage:
+//    theta^k is quantised once per iteration to T_i = round(theta_i / delta),
+//    delta = 2^e with |T_i| <= 2^28, and split into four signed base-256 digits
+//    d_0..d_3 (T = d0*2^24 + d1*2^16 + d2*2^8 + d3).  Each digit row is an int8
+//    B operand; D_jk = sum_i G_ij d_k(i) is an exact int32 (tcgen05 kind::i8
+//    accumulator or dp4a), so sum_i (G_ij - m_j) T_i = (n*S_j - colsum_j*sum T)/n
+//    is exact and order-independent; g_j = delta * that / s_j in fp64.
+//  * a4 (X~ beta) accumulates int64 fixed-point C_j = round(2^E beta_j / s_j)
+//    with E chosen from max|C| and |S| so nothing overflows; integer atomics
+//    make the result independent of scheduling (bitwise deterministic).
+//  * proxes, residuals, dual step and all reductions are fp64.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define FSQR_NPART 5          // per-CTA K2 partials per RHS: rb, bb, gg, pen, nnz
+#define FSQR_NSCAL 4          // per-RHS scalars of the current iterate: Rp, Rz, loss_sum, (spare)
+#define FSQR_MAXR 16
+#define FSQR_TRACE_W 5        // trace row: Rp, Rb, Rz, obj, nnz
+#define FSQR_PATH_W 7         // path record: iters, Rp, Rb, Rz, obj, nnz, converged
+
+enum { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_NUMERIC = 3 };
+
+struct Dev {
+  // sizes / layout
+  int n, R, G, storage, npad, ldk;
+  int64_t p, ld;
+  int64_t gq, grem;                 // block partition of the p+1 model columns: q = (p+1)/G, rem
+  // design (borrowed) + statistics
+  const uint8_t* X8;
+  const float* Xf;
+  const int32_t* colsum;            // exact integer column sums (genotype storage)
+  const double* mean;
+  const double* inv_sd;
+  const double* lamw;               // [p+1] or nullptr
+  const double* eta;                // [G]
+  // state
+  double* beta[2];                  // [(p+1)*R], coefficient-major
+  double* z;                        // [R*n]
+  double* theta;                    // [R*n]
+  double* rres;                     // [R*n] r^k
+  double* s;                        // [R*n] X~beta^k
+  const double* y;                  // [n]
+  double* sdense;                   // [R*n] forward output of the fp32 path
+  int8_t* Bq;                       // [npad][ldk] theta digits
+  long long* Tsum;                  // [R]
+  double* delta;                    // [R]
+  double* sumth;                    // [R] sum theta^k (fp64)
+  // support lists, double-buffered by iteration parity
+  int32_t* sup_idx[2];              // data column index
+  double* sup_c[2];                 // [cap*R] beta_j / s_j
+  double* sup_b[2];                 // [cap*R] beta_j
+  int* sup_cnt;                     // [2]
+  unsigned long long* cmax;         // [2][R] bits of max |beta_j/s_j|
+  long long* sacc;                  // [R*n] int64 forward accumulators
+  long long* mterm;                 // [R]
+  // K2 partials + last-CTA ticket
+  double* k2part;                   // [grid][R][FSQR_NPART]
+  unsigned int* ticket;
+  // per-RHS control
+  const double* tau;                // [R]
+  double* lam_cur;                  // [R]
+  double* scal;                     // [R][FSQR_NSCAL]
+  int* status;                      // [R]
+  long long* commit_iter;           // [R]
+  long long* iter;                  // [1]
+  int* stop;                        // [1]
+  double* lastR;                    // [R][FSQR_TRACE_W]
+  double* trace;                    // [trace_cap][R][FSQR_TRACE_W]
+  int trace_cap;
+  double tol, mu, sigma;            // sigma = mu/(G+1)
+  long long max_iter;
+  // path
+  const double* lam_path;           // [R][T]
+  int T;
+  int* t_idx;                       // [R]
+  long long* pt_iters;              // [R]
+  long long max_iter_point;
+  double* path_rec;                 // [R][T][FSQR_PATH_W]
+  int32_t* path_idx;                // [R][T][path_cap]
+  double* path_beta;                // [R][T][path_cap]
+  long long* path_cnt;              // [R][T]
+  int path_cap;
+  // mode (baked per captured graph)
+  int check;                        // stop test on
+  int path;                         // lambda-path state machine on
+  int update;                       // 0: K2 computes R(w^k) only (fsqr_kkt)
+};
+
+// ------------------------------------------------------------------ helpers
+
+__device__ __forceinline__ int block_of_col(const Dev& D, int64_t j) {
+  // contiguous near-equal blocks of the p+1 model columns (first `grem` blocks hold q+1)
+  int64_t big = D.grem * (D.gq + 1);
+  return (int)(j < big ? j / (D.gq + 1) : D.grem + (j - big) / D.gq);
+}
+
+__device__ __forceinline__ double pos_part(double v) { return v > 0.0 ? v : 0.0; }
+
+// E14
+__device__ __forceinline__ double prox_beta(double b, double g, double lam, double eta) {
+  double a = eta * b + g;
+  return (pos_part(a - lam) - pos_part(-a - lam)) / eta;
+}
+
+// soft-threshold S_c(v) for the KKT residual
+__device__ __forceinline__ double soft_thr(double v, double c) {
+  return v > c ? v - c : (v < -c ? v + c : 0.0);
+}
+
+// prox of rho_tau with unit weight (KKT residual R_z)
+__device__ __forceinline__ double prox_rho1(double v, double tau) {
+  return v > tau ? v - tau : (v < tau - 1.0 ? v + 1.0 - tau : 0.0);
+}
+
+// fixed-point exponent for the forward product: 2 n cnt max|c| 2^E < 2^61
+__device__ __forceinline__ int fwd_exponent(double cmax, long long cnt, int n) {
+  if (!(cmax > 0.0) || cnt <= 0) return 0;
+  int e;
+  frexp(2.0 * (double)n * (double)cnt * cmax, &e);
+  return 61 - e;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ------------------------------------------------------------------ PTX: mbarrier / TMA / tcgen05
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, uint64_t* bar, int x, int y,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void prefetch_tmap(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// SM100 shared-memory matrix descriptor, K-major, 128B swizzle: SBO = 1024 B (8 rows x 128 B), LBO = 16 B
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;               // LBO (unused for swizzled K-major) = 16 B
+  d |= (uint64_t)(1024u >> 4) << 32;     // SBO
+  d |= (uint64_t)1u << 46;               // version = 1 (sm100)
+  d |= (uint64_t)2u << 61;               // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor: kind::i8, D = s32, A = s8, B = s8, both K-major, M = 128, N = npad
+__host__ __device__ constexpr uint32_t idesc_i8(int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// ------------------------------------------------------------------ per-launch K2 context
+
+template <int RMAX>
+struct K2Ctx {
+  long long k;
+  const double* beta_in;
+  double* beta_out;
+  int32_t* sidx;
+  double* sc;
+  double* sb;
+  int* scnt;
+  int R;
+  bool active[RMAX];
+  double lam[RMAX];
+  double gscale[RMAX];      // delta_r / n (genotype storage)
+  long long Tsum[RMAX];
+};
+
+// per-thread fp64 partials
+template <int RMAX>
+struct K2Part {
+  double v[RMAX][FSQR_NPART];
+  double cmax[RMAX];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) {
+      cmax[r] = 0.0;
+#pragma unroll
+      for (int q = 0; q < FSQR_NPART; ++q) v[r][q] = 0.0;
+    }
+  }
+};
+
+// a2 epilogue for one data column c with g_r = (X~^T theta^k)_j, j = c + 1.
+// Writes beta^{k+1}, accumulates R_beta(w^k) partials and the penalty of beta^k,
+// returns whether beta^{k+1}_j != 0 for some active RHS (support membership) and
+// fills cval/bval for the support entry.
+template <int RMAX>
+__device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, int64_t c, const double* g,
+                                           K2Part<RMAX>& P, double* cval, double* bval) {
+  const int64_t j = c + 1;
+  const double isd = D.inv_sd[c];
+  const double w = D.lamw ? D.lamw[j] : 1.0;
+  const double eta = D.eta[block_of_col(D, j)];
+  bool nz = false;
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) {
+    cval[r] = 0.0;
+    bval[r] = 0.0;
+    if (r >= C.R || !C.active[r]) continue;
+    const double b = C.beta_in[j * C.R + r];
+    const double lam = C.lam[r] * w;
+    // KKT residual part of w^k and penalty at beta^k
+    const double d = b - soft_thr(b + g[r], lam);
+    P.v[r][0] += d * d;
+    P.v[r][1] += b * b;
+    P.v[r][2] += g[r] * g[r];
+    P.v[r][3] += lam * fabs(b);
+    P.v[r][4] += (b != 0.0) ? 1.0 : 0.0;
+    if (D.update) {
+      const double bn = prox_beta(b, g[r], lam, eta);
+      C.beta_out[j * C.R + r] = bn;
+      if (bn != 0.0) {
+        nz = true;
+        const double cv = bn * isd;
+        cval[r] = cv;
+        bval[r] = bn;
+        P.cmax[r] = fmax(P.cmax[r], fabs(cv));
+      }
+    }
+  }
+  return nz;
+}
+
+// warp-aggregated append of support entries (lanes with nz)
+template <int RMAX>
+__device__ __forceinline__ void support_append(const K2Ctx<RMAX>& C, bool nz, int64_t c, const double* cval,
+                                               const double* bval) {
+  const unsigned m = __ballot_sync(0xffffffffu, nz);
+  if (m == 0) return;
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  if (lane == __ffs(m) - 1) base = atomicAdd(C.scnt, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+  if (nz) {
+    const int e = base + __popc(m & ((1u << lane) - 1u));
+    C.sidx[e] = (int32_t)c;
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) {
+      if (r < C.R) {
+        C.sc[(int64_t)e * C.R + r] = cval[r];
+        C.sb[(int64_t)e * C.R + r] = bval[r];
+      }
+    }
+  }
+}
+
+// exact integer reconstruction of g_r from the four digit accumulators of RHS r
+__device__ __forceinline__ double g_from_digits(int n, int32_t colsum, long long Tsum, double gscale, double isd,
+                                                const int32_t* Dk) {
+  long long S = ((long long)Dk[0] << 24) + ((long long)Dk[1] << 16) + ((long long)Dk[2] << 8) + (long long)Dk[3];
+  long long num = (long long)n * S - (long long)colsum * Tsum;
+  return (double)num * gscale * isd;
+}
+
+// ------------------------------------------------------------------ host launchers (one per TU)
+
+struct LaunchCfg {
+  int grid;
+  cudaStream_t st;
+};
+
+void launch_k2_tc(const Dev& D, const void* tmX, const void* tmB, int grid, cudaStream_t st);
+void launch_k2_simt(const Dev& D, int grid, cudaStream_t st);
+void launch_k1(const Dev& D, int grid, cudaStream_t st);
+void launch_finalize(const Dev& D, cudaStream_t st);
+int k2_tc_smem_bytes(int npad);
+cudaError_t k2_tc_init();
+int k2_tc_supported(int npad);

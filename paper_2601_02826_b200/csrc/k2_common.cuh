@@ -1,0 +1,183 @@
+// k2_common.cuh — end-of-pass logic shared by the X~^T theta kernels (TC and SIMT):
+// CTA reduction of the a2/a6 partials, last-CTA convergence test (a6) and the
+// per-RHS lambda-path state machine (a8).
+#pragma once
+#include "fsqr_dev.cuh"
+
+template <int RMAX>
+__device__ void k2_load_ctx(const Dev& D, K2Ctx<RMAX>& C) {
+  C.k = *D.iter;
+  const int par = (int)(C.k & 1);
+  C.beta_in = D.beta[par];
+  C.beta_out = D.beta[par ^ 1];
+  C.sidx = D.sup_idx[par ^ 1];
+  C.sc = D.sup_c[par ^ 1];
+  C.sb = D.sup_b[par ^ 1];
+  C.scnt = D.sup_cnt + (par ^ 1);
+  C.R = D.R;
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) {
+    const bool a = r < D.R && D.status[r] == ST_ACTIVE;
+    C.active[r] = a;
+    C.lam[r] = r < D.R ? D.lam_cur[r] : 0.0;
+    C.gscale[r] = r < D.R ? D.delta[r] / (double)D.n : 0.0;
+    C.Tsum[r] = r < D.R ? D.Tsum[r] : 0;
+  }
+}
+
+// Block reduction of the per-thread partials (fixed order), publication of the
+// CTA partials, and, in the last CTA to finish, the a6 test.  Must be called by
+// every thread of the block; `red` needs blockDim/32 * RMAX * (NPART+1) doubles.
+template <int RMAX>
+__device__ void k2_finish(const Dev& D, const K2Ctx<RMAX>& C, K2Part<RMAX>& P, double* red) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  constexpr int W = FSQR_NPART + 1;
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) {
+    if (r >= C.R) break;
+#pragma unroll
+    for (int q = 0; q < FSQR_NPART; ++q) {
+      double v = warp_sum_d(P.v[r][q]);
+      if (lane == 0) red[(wid * RMAX + r) * W + q] = v;
+    }
+    double m = P.cmax[r];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) red[(wid * RMAX + r) * W + FSQR_NPART] = m;
+  }
+  __syncthreads();
+  __shared__ bool s_last;
+  if (tid < C.R) {
+    const int r = tid;
+    double acc[FSQR_NPART] = {0, 0, 0, 0, 0};
+    double m = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      for (int q = 0; q < FSQR_NPART; ++q) acc[q] += red[(w * RMAX + r) * W + q];
+      m = fmax(m, red[(w * RMAX + r) * W + FSQR_NPART]);
+    }
+    for (int q = 0; q < FSQR_NPART; ++q) D.k2part[((size_t)blockIdx.x * D.R + r) * FSQR_NPART + q] = acc[q];
+    if (D.update && m > 0.0)
+      atomicMax(D.cmax + (size_t)((C.k + 1) & 1) * D.R + r, (unsigned long long)__double_as_longlong(m));
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned t = atomicAdd(D.ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+
+  // ---------------- last CTA: R(w^k) for every active RHS (fixed-order sum over CTAs)
+  __shared__ int s_rec[FSQR_MAXR];
+  if (tid < C.R) {
+    const int r = tid;
+    s_rec[r] = -1;
+    if (C.active[r]) {
+      double a[FSQR_NPART] = {0, 0, 0, 0, 0};
+      for (int b = 0; b < (int)gridDim.x; ++b)
+        for (int q = 0; q < FSQR_NPART; ++q) a[q] += D.k2part[((size_t)b * D.R + r) * FSQR_NPART + q];
+      const double g0 = D.sumth[r], b0 = C.beta_in[r];
+      const double rb = a[0] + g0 * g0, bb = a[1] + b0 * b0, gg = a[2] + g0 * g0;
+      const double Rb = sqrt(rb) / (1.0 + sqrt(bb) + sqrt(gg));
+      const double* sc = D.scal + r * FSQR_NSCAL;
+      const double Rp = sc[0], Rz = sc[1];
+      const double obj = sc[2] / (double)D.n + a[3];
+      double* lr = D.lastR + r * FSQR_TRACE_W;
+      lr[0] = Rp;
+      lr[1] = Rb;
+      lr[2] = Rz;
+      lr[3] = obj;
+      lr[4] = a[4];
+      if (D.update) {
+        double* tr = D.trace + ((size_t)(C.k % D.trace_cap) * D.R + r) * FSQR_TRACE_W;
+        for (int q = 0; q < FSQR_TRACE_W; ++q) tr[q] = lr[q];
+        const double Rm = fmax(Rp, fmax(Rb, Rz));
+        const bool fin = isfinite(Rp) && isfinite(Rb) && isfinite(Rz) && isfinite(obj);
+        if (!fin) {
+          D.status[r] = ST_NUMERIC;
+          D.commit_iter[r] = C.k;
+        } else if (D.path) {
+          const bool conv = Rm <= D.tol;
+          const long long it = D.pt_iters[r];
+          if (conv || it >= D.max_iter_point) {
+            const int t = D.t_idx[r];
+            double* pr = D.path_rec + ((size_t)r * D.T + t) * FSQR_PATH_W;
+            pr[0] = (double)it;
+            pr[1] = Rp;
+            pr[2] = Rb;
+            pr[3] = Rz;
+            pr[4] = obj;
+            pr[5] = a[4];
+            pr[6] = conv ? 1.0 : 0.0;
+            s_rec[r] = t;
+            if (t == D.T - 1) {
+              D.status[r] = conv ? ST_CONVERGED : ST_MAXITER;
+              D.commit_iter[r] = C.k;
+            } else {
+              D.t_idx[r] = t + 1;
+              D.lam_cur[r] = D.lam_path[(size_t)r * D.T + t + 1];
+              D.pt_iters[r] = 0;
+            }
+          } else {
+            D.pt_iters[r] = it + 1;
+          }
+        } else if (D.check) {
+          if (Rm <= D.tol) {
+            D.status[r] = ST_CONVERGED;
+            D.commit_iter[r] = C.k;
+          } else if (C.k >= D.max_iter) {
+            D.status[r] = ST_MAXITER;
+            D.commit_iter[r] = C.k;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // ---------------- path: copy the sparse solution beta^k (support list of parity k) of recorded RHS
+  if (D.update && D.path) {
+    const int par = (int)(C.k & 1);
+    const int cnt = D.sup_cnt[par];
+    __shared__ int s_cnt;
+    for (int r = 0; r < C.R; ++r) {
+      const int t = s_rec[r];
+      if (t < 0) continue;
+      if (tid == 0) s_cnt = 1;
+      __syncthreads();
+      const size_t base = ((size_t)r * D.T + t) * D.path_cap;
+      if (tid == 0) {
+        D.path_idx[base] = 0;
+        D.path_beta[base] = C.beta_in[r];
+      }
+      for (int e0 = 0; e0 < cnt; e0 += blockDim.x) {
+        const int e = e0 + tid;
+        double bv = 0.0;
+        int jj = 0;
+        if (e < cnt) {
+          bv = D.sup_b[par][(size_t)e * D.R + r];
+          jj = D.sup_idx[par][e] + 1;
+        }
+        if (bv != 0.0) {
+          const int slot = atomicAdd(&s_cnt, 1);
+          if (slot < D.path_cap) {
+            D.path_idx[base + slot] = jj;
+            D.path_beta[base + slot] = bv;
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) D.path_cnt[(size_t)r * D.T + t] = s_cnt;
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    if (D.update) {
+      int any = 0;
+      for (int r = 0; r < D.R; ++r) any |= (D.status[r] == ST_ACTIVE);
+      *D.stop = any ? 0 : 1;
+    }
+    *D.ticket = 0u;
+  }
+}

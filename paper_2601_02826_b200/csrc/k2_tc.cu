@@ -1,0 +1,230 @@
+// k2_tc.cu — a1+a2 on the 5th-generation tensor cores (sm_100a).
+//
+// One outer FS-QRPPA iteration streams the whole genotype matrix once through
+// this kernel: g^k = X~^T theta^k (PAPER.md:L392,
+// "matrix-vector products ... X^T theta"), then the weighted soft-threshold prox
+// beta^{k+1} = E14(beta^k, g^k) (L274-277), the support list of beta^{k+1}, and
+// the R_beta(w^k) / penalty partials of the stopping test.
+//
+// Mapping: X is stored SNP-major (column c = n contiguous bytes), which is
+// exactly the K-major A operand of D[c, q] = sum_i X[i, c] * B[i, q] with
+// M = 128 columns per tile, K = n samples and N = npad digit rows of theta.
+// Persistent CTAs (one per SM) walk tiles of 128 columns; a TMA producer warp
+// streams 128x128-byte A boxes (SWIZZLE_128B) plus the matching B box through
+// an mbarrier ring; one elected thread issues tcgen05.mma kind::i8 into a
+// double-buffered int32 TMEM accumulator; four epilogue warps (one per TMEM
+// lane quarter) read the exact digit sums with tcgen05.ld and run the fp64
+// epilogue while the next tile accumulates.  X is read from HBM exactly once
+// per iteration with an evict-first L2 policy; B (theta digits, <= 1.3 MB) is
+// L2-resident and re-read per stage with evict-last.
+#include <cuda.h>
+
+#include "k2_common.cuh"
+
+namespace {
+
+constexpr int TILE_M = 128;   // columns per tile (UMMA M)
+constexpr int TILE_K = 128;   // bytes of K per stage (one 128B swizzle row)
+constexpr int A_BYTES = TILE_M * TILE_K;
+constexpr int THREADS = 256;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4..7 epilogue
+
+template <int NPAD>
+struct Cfg {
+  static constexpr int B_BYTES = NPAD * TILE_K;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE;
+  static constexpr int RMAX = NPAD / 4;
+  static constexpr int TMEM_COLS = (2 * NPAD <= 32) ? 32 : (2 * NPAD <= 64 ? 64 : (2 * NPAD <= 128 ? 128 : 256));
+  static constexpr int RED_DOUBLES = (THREADS / 32) * RMAX * (FSQR_NPART + 1);
+  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE + 1024 /*barriers*/ + RED_DOUBLES * 8;
+};
+
+template <int NPAD>
+__global__ void __launch_bounds__(THREADS, 1)
+    k2_tc_kernel(const Dev D, const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmB) {
+  using CF = Cfg<NPAD>;
+  constexpr int RMAX = CF::RMAX;
+  if (*D.stop) return;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + CF::STAGES * A_BYTES;
+  uint64_t* full = (uint64_t*)(smem + CF::STAGES * CF::STAGE);
+  uint64_t* empty = full + CF::STAGES;
+  uint64_t* tfull = empty + CF::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  double* red = (double*)(smem + CF::STAGES * CF::STAGE + 1024);
+
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int64_t ntiles = (D.p + TILE_M - 1) / TILE_M;
+  const int kblocks = (D.n + TILE_K - 1) / TILE_K;
+
+  K2Ctx<RMAX> C;
+  k2_load_ctx(D, C);
+  K2Part<RMAX> P;
+  P.zero();
+
+  if (wid == 0 && lane == 0) {
+    prefetch_tmap(&tmX);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < CF::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+  }
+  if (wid == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(CF::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (wid == 0) {
+    // ===== TMA producer =====
+    if (lane == 0) {
+      const uint64_t pol_x = policy_evict_first(), pol_b = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], (uint32_t)CF::STAGE);
+          tma_load_2d(sA + stage * A_BYTES, &tmX, &full[stage], kb * TILE_K, (int)(t * TILE_M), pol_x);
+          tma_load_2d(sB + stage * CF::B_BYTES, &tmB, &full[stage], kb * TILE_K, 0, pol_b);
+          if (++stage == CF::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (wid == 1) {
+    // ===== MMA issuer (single thread) =====
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_i8(NPAD);
+      int stage = 0;
+      uint32_t phase = 0;
+      int lt = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+        const int acc = lt & 1;
+        const uint32_t aph = (lt >> 1) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * NPAD);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = umma_desc_sw128(smem_u32(sA + stage * A_BYTES));
+          const uint64_t bdesc = umma_desc_sw128(smem_u32(sB + stage * CF::B_BYTES));
+#pragma unroll
+          for (int k = 0; k < TILE_K / 32; ++k)   // K = 32 bytes per kind::i8 MMA
+            umma_i8(d_tmem, adesc + (uint64_t)(2 * k), bdesc + (uint64_t)(2 * k), idesc, (kb | k) != 0);
+          umma_commit(&empty[stage]);
+          if (++stage == CF::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else if (wid >= 4) {
+    // ===== epilogue: TMEM lanes 32*(wid-4) .. +31 = columns of the tile =====
+    const int q = wid - 4;
+    int lt = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+      const int acc = lt & 1;
+      const uint32_t aph = (lt >> 1) & 1;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      int32_t dv[NPAD];
+#pragma unroll
+      for (int h = 0; h < NPAD / 16; ++h) {
+        uint32_t v[16];
+        tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NPAD + h * 16), v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 16; ++u) dv[h * 16 + u] = (int32_t)v[u];
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+
+      const int64_t c = t * TILE_M + q * 32 + lane;
+      bool nz = false;
+      double cval[RMAX], bval[RMAX];
+      if (c < D.p) {
+        double g[RMAX];
+        const int32_t cs = D.colsum[c];
+        const double isd = D.inv_sd[c];
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r)
+          g[r] = r < C.R ? g_from_digits(D.n, cs, C.Tsum[r], C.gscale[r], isd, dv + 4 * r) : 0.0;
+        nz = epi_column<RMAX>(D, C, c, g, P, cval, bval);
+      } else {
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r) cval[r] = bval[r] = 0.0;
+      }
+      if (D.update) support_append<RMAX>(C, nz, c, cval, bval);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (wid == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(CF::TMEM_COLS)
+                 : "memory");
+  }
+  k2_finish<RMAX>(D, C, P, red);
+}
+
+template <int NPAD>
+void launch_np(const Dev& D, const void* tmX, const void* tmB, int grid, cudaStream_t st) {
+  using CF = Cfg<NPAD>;
+  k2_tc_kernel<NPAD><<<grid, THREADS, CF::SMEM, st>>>(D, *(const CUtensorMap*)tmX, *(const CUtensorMap*)tmB);
+}
+
+template <int NPAD>
+cudaError_t init_np() {
+  return cudaFuncSetAttribute(k2_tc_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<NPAD>::SMEM);
+}
+
+}  // namespace
+
+cudaError_t k2_tc_init() {
+  cudaError_t e;
+  if ((e = init_np<16>()) != cudaSuccess) return e;
+  if ((e = init_np<32>()) != cudaSuccess) return e;
+  if ((e = init_np<48>()) != cudaSuccess) return e;
+  return init_np<64>();
+}
+
+int k2_tc_supported(int npad) { return npad == 16 || npad == 32 || npad == 48 || npad == 64; }
+
+int k2_tc_smem_bytes(int npad) {
+  switch (npad) {
+    case 16: return Cfg<16>::SMEM;
+    case 32: return Cfg<32>::SMEM;
+    case 48: return Cfg<48>::SMEM;
+    default: return Cfg<64>::SMEM;
+  }
+}
+
+void launch_k2_tc(const Dev& D, const void* tmX, const void* tmB, int grid, cudaStream_t st) {
+  switch (D.npad) {
+    case 16: launch_np<16>(D, tmX, tmB, grid, st); break;
+    case 32: launch_np<32>(D, tmX, tmB, grid, st); break;
+    case 48: launch_np<48>(D, tmX, tmB, grid, st); break;
+    default: launch_np<64>(D, tmX, tmB, grid, st); break;
+  }
+}

@@ -1,0 +1,527 @@
+// kfin.cu — a3 + a5 + a6 (n-vector part) and the setup kernels.
+//
+// finalize (one CTA, 1024 threads, fixed-order reductions):
+//   s^{k+1}_i = 2^-E (n S_i - M)/n + beta_0^{k+1}       (a4 result, intercept added here)
+//   z^{k+1}   = E15(z^k, theta^k)
+//   r^{k+1}   = s^{k+1} + z^{k+1} - y
+//   theta^{k+1} = theta^k - mu/(G+1) (2 r^{k+1} - r^k)   E12, L253-254
+//   R_p, R_z (w^{k+1}), loss, sum theta, and the digit planes of theta^{k+1}
+//   for the next X~^T theta pass.
+// Setup: column statistics (a0), power method pieces (a0'), lambda_max, state init.
+#include "fsqr_dev.cuh"
+
+namespace {
+
+constexpr int FT = 1024;
+
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    const double x = warp_sum_d(v[q]);
+    if (lane == 0) sm[wid * NV + q] = x;
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double x = lane < nw ? sm[lane * NV + q] : 0.0;
+      x = warp_sum_d(x);
+      if (lane == 0) sm[32 * NV + q] = x;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) v[q] = sm[32 * NV + q];
+  __syncthreads();
+}
+
+__device__ __forceinline__ long long block_sum_ll(long long v, long long* sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) sm[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    long long x = lane < nw ? sm[lane] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) sm[32] = x;
+  }
+  __syncthreads();
+  const long long r = sm[32];
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ double block_max(double v, double* sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (lane == 0) sm[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    double x = lane < nw ? sm[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+    if (lane == 0) sm[32] = x;
+  }
+  __syncthreads();
+  const double r = sm[32];
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ double rho_tau(double u, double tau) { return (tau - (u < 0.0 ? 1.0 : 0.0)) * u; }
+
+// theta -> balanced base-256 digit planes (rows 4r..4r+3 of Bq); returns sum T (exact)
+__device__ void quantize_theta(const Dev& D, int r, double mx, long long* smll) {
+  const int n = D.n;
+  int ex = 0;
+  double dlt = 1.0;
+  if (mx > 0.0 && isfinite(mx)) {
+    frexp(mx, &ex);          // mx < 2^ex
+    dlt = ldexp(1.0, ex - 28);
+  }
+  const double inv = 1.0 / dlt;  // exact (power of two)
+  long long ts = 0;
+  int8_t* b0 = D.Bq + (int64_t)(4 * r) * D.ldk;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double th = D.theta[(int64_t)r * n + i];
+    long long T = isfinite(th) ? __double2ll_rn(th * inv) : 0;
+    ts += T;
+    const int d3 = (int)(int8_t)(T & 0xFF);
+    T = (T - d3) >> 8;
+    const int d2 = (int)(int8_t)(T & 0xFF);
+    T = (T - d2) >> 8;
+    const int d1 = (int)(int8_t)(T & 0xFF);
+    T = (T - d1) >> 8;
+    b0[i] = (int8_t)T;
+    b0[D.ldk + i] = (int8_t)d1;
+    b0[2 * D.ldk + i] = (int8_t)d2;
+    b0[3 * D.ldk + i] = (int8_t)d3;
+  }
+  ts = block_sum_ll(ts, smll);
+  if (threadIdx.x == 0) {
+    D.Tsum[r] = ts;
+    D.delta[r] = dlt;
+  }
+}
+
+// shared n-vector step: from s (already including beta_0), update z, theta, r and the per-RHS scalars
+// mode 0: iteration (a3+a5), mode 1: state init (z, theta given; only r and the scalars)
+__device__ void nvec_step(const Dev& D, int r, int mode, double b0, int fwd_par, double* smd, long long* smll) {
+  const int n = D.n;
+  const double tau = D.tau[r];
+  const double mu = D.mu, sig = D.sigma;
+  const double tn = tau / ((double)n * mu), un = (1.0 - tau) / ((double)n * mu);
+  int E = 0;
+  long long mt = 0;
+  if (D.storage != 0) {
+    const int cnt = D.sup_cnt[fwd_par];
+    const double cm = __longlong_as_double((long long)D.cmax[fwd_par * D.R + r]);
+    E = fwd_exponent(cm, cnt, n);
+    mt = D.mterm[r];
+  }
+  const double inv_scale = ldexp(1.0, -E);
+  double acc[7] = {0, 0, 0, 0, 0, 0, 0};  // rr, zz, tt, rzz, loss, sumth, yy
+  double mx = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int64_t o = (int64_t)r * n + i;
+    double sv;
+    if (D.storage == 0) {
+      sv = D.sdense[o] + b0;
+    } else {
+      sv = (double)((long long)n * D.sacc[o] - mt) * inv_scale / (double)n + b0;
+      D.sacc[o] = 0;
+    }
+    const double yi = D.y[i];
+    double zn, thn;
+    if (mode == 0) {
+      const double zo = D.z[o], th = D.theta[o], ro = D.rres[o];
+      zn = pos_part(zo + th / mu - tn) - pos_part(-zo - th / mu - un);   // E15
+      const double rn = sv + zn - yi;
+      thn = th - sig * (2.0 * rn - ro);                                   // E12
+      D.z[o] = zn;
+      D.theta[o] = thn;
+      D.rres[o] = rn;
+      acc[0] += rn * rn;
+    } else {
+      zn = D.z[o];
+      thn = D.theta[o];
+      const double rn = sv + zn - yi;
+      D.rres[o] = rn;
+      acc[0] += rn * rn;
+    }
+    D.s[o] = sv;
+    const double nt = (double)n * thn;
+    const double dz = zn - prox_rho1(zn + nt, tau);
+    acc[1] += zn * zn;
+    acc[2] += nt * nt;
+    acc[3] += dz * dz;
+    acc[4] += rho_tau(yi - sv, tau);
+    acc[5] += thn;
+    acc[6] += yi * yi;
+    mx = fmax(mx, fabs(thn));
+    if (!isfinite(thn)) mx = thn;
+  }
+  block_sum<7>(acc, smd);
+  mx = block_max(mx, smd);
+  if (threadIdx.x == 0) {
+    double* sc = D.scal + r * FSQR_NSCAL;
+    sc[0] = sqrt(acc[0]) / (1.0 + sqrt(acc[6]));
+    sc[1] = sqrt(acc[3]) / (1.0 + sqrt(acc[1]) + sqrt(acc[2]));
+    sc[2] = acc[4];
+    sc[3] = acc[6];
+    D.sumth[r] = acc[5];
+    D.mterm[r] = 0;
+  }
+  if (D.storage != 0) quantize_theta(D, r, mx, smll);
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(FT) k_finalize(const Dev D) {
+  __shared__ double smd[32 * 8 + 8];
+  __shared__ long long smll[33];
+  if (*D.stop) return;
+  const long long k = *D.iter;
+  const int par = (int)(k & 1), par1 = par ^ 1;
+  for (int r = 0; r < D.R; ++r) {
+    if (D.status[r] != ST_ACTIVE) continue;
+    // intercept: lambda_0 = 0, so E14 gives beta_0 + g_0/eta_1 with g_0 = sum theta^k
+    const double b0 = D.beta[par][r] + D.sumth[r] / D.eta[0];
+    if (threadIdx.x == 0) D.beta[par1][r] = b0;
+    nvec_step(D, r, 0, b0, par1, smd, smll);
+  }
+  __syncthreads();
+  if (threadIdx.x < D.R) D.cmax[par * D.R + threadIdx.x] = 0ull;
+  if (threadIdx.x == 0) {
+    D.sup_cnt[par] = 0;
+    *D.iter = k + 1;
+  }
+}
+
+// state init after create / set_state: s from the support list of the current parity (k1 in cur mode)
+__global__ void __launch_bounds__(FT) k_init_state(const Dev D) {
+  __shared__ double smd[32 * 8 + 8];
+  __shared__ long long smll[33];
+  const long long k = *D.iter;
+  const int par = (int)(k & 1);
+  for (int r = 0; r < D.R; ++r) nvec_step(D, r, 1, D.beta[par][r], par, smd, smll);
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- setup kernels
+
+template <int ST>
+__global__ void k_colstats_int(const Dev D, int32_t* colsum, double* mean, double* inv_sd, double* sd, int* bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = gw; c < D.p; c += nw) {
+    const uint8_t* col = D.X8 + c * D.ld;
+    long long s1 = 0, s2 = 0;
+    for (int i = lane; i < D.n; i += 32) {
+      const int g = ST == 1 ? col[i] : (col[i >> 2] >> (2 * (i & 3))) & 3;
+      s1 += g;
+      s2 += g * g;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane == 0) {
+      const long long n = D.n;
+      const long long num = n * s2 - s1 * s1;   // n(n-1) * sample variance, exact
+      colsum[c] = (int32_t)s1;
+      mean[c] = (double)s1 / (double)n;
+      const double v = (double)num / ((double)n * (double)(n - 1));
+      const double s = sqrt(v);
+      sd[c] = s;
+      inv_sd[c] = 1.0 / s;
+      if (num <= 0) atomicMin(bad, (int)c);
+    }
+  }
+}
+
+__global__ void k_colstats_f32(const Dev D, double* mean, double* inv_sd, double* sd, int* bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = gw; c < D.p; c += nw) {
+    const float* col = D.Xf + c * D.ld;
+    double s1 = 0.0;
+    for (int i = lane; i < D.n; i += 32) s1 += (double)col[i];
+    s1 = warp_sum_d(s1);
+    const double m = s1 / (double)D.n;
+    double s2 = 0.0;
+    for (int i = lane; i < D.n; i += 32) {
+      const double d = (double)col[i] - m;
+      s2 += d * d;
+    }
+    s2 = warp_sum_d(s2);
+    if (lane == 0) {
+      const double s = sqrt(s2 / (double)(D.n - 1));
+      mean[c] = m;
+      sd[c] = s;
+      inv_sd[c] = 1.0 / s;
+      if (!(s > 0.0)) atomicMin(bad, (int)c);
+    }
+  }
+}
+
+__device__ __forceinline__ double xt_raw(const Dev& D, int64_t c, int i) {
+  if (D.storage == 0) return (double)D.Xf[c * D.ld + i];
+  if (D.storage == 1) return (double)D.X8[c * D.ld + i];
+  return (double)((D.X8[c * D.ld + (i >> 2)] >> (2 * (i & 3))) & 3);
+}
+
+// power method start vector: 2U - 1, U from the splitmix64 finaliser keyed by (seed, j)
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__global__ void k_power_start(int64_t p1, uint64_t seed, double* v) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p1; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t h = mix64(seed ^ mix64((uint64_t)j));
+    v[j] = 2.0 * ((double)(h >> 11) * 0x1.0p-53) - 1.0;
+  }
+}
+
+// u[g][i] = sum_{j in block g} x~_ij v_j (ascending j), thread per (i, g)
+__global__ void k_power_fwd(const Dev D, const int64_t* bstart, const double* v, const int* frozen, double* u) {
+  const int g = blockIdx.y;
+  if (frozen[g]) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= D.n) return;
+  const int64_t j0 = bstart[g], j1 = bstart[g + 1];
+  double a = 0.0;
+  for (int64_t j = j0; j < j1; ++j) {
+    const double vj = v[j];
+    if (j == 0) {
+      a = fma(1.0, vj, a);
+      continue;
+    }
+    const int64_t c = j - 1;
+    a = fma((xt_raw(D, c, i) - D.mean[c]) * D.inv_sd[c], vj, a);
+  }
+  u[(int64_t)g * D.n + i] = a;
+}
+
+// w_j = sum_i x~_ij u_{g(j), i}  (warp per model column, fixed butterfly); optional max |w_j| (j >= 1)
+__global__ void k_back_f64(const Dev D, const double* u, int per_block, const int* frozen, double* w,
+                           unsigned long long* maxbits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = gw; j <= D.p; j += nw) {
+    const int g = per_block ? block_of_col(D, j) : 0;
+    if (frozen && frozen[g]) continue;
+    const double* ug = u + (int64_t)g * D.n;
+    double a = 0.0;
+    if (j == 0) {
+      for (int i = lane; i < D.n; i += 32) a += ug[i];
+    } else {
+      const int64_t c = j - 1;
+      const double m = D.mean[c], isd = D.inv_sd[c];
+      for (int i = lane; i < D.n; i += 32) a = fma((xt_raw(D, c, i) - m) * isd, ug[i], a);
+    }
+    a = warp_sum_d(a);
+    if (lane == 0) {
+      if (w) w[j] = a;
+      if (maxbits && j >= 1) atomicMax(maxbits, (unsigned long long)__double_as_longlong(fabs(a)));
+    }
+  }
+}
+
+// per block g: est = v_g . w_g, nrm = ||w_g||  (one CTA per block, fixed order)
+__global__ void k_power_reduce(const int64_t* bstart, const double* v, const double* w, const int* frozen,
+                               double* est, double* nrm) {
+  __shared__ double sm[32 * 2 + 2];
+  const int g = blockIdx.x;
+  if (frozen[g]) return;
+  double a[2] = {0.0, 0.0};
+  for (int64_t j = bstart[g] + threadIdx.x; j < bstart[g + 1]; j += blockDim.x) {
+    a[0] += v[j] * w[j];
+    a[1] += w[j] * w[j];
+  }
+  block_sum<2>(a, sm);
+  if (threadIdx.x == 0) {
+    est[g] = a[0];
+    nrm[g] = sqrt(a[1]);
+  }
+}
+
+// v_j <- w_j / ||w_g||  (or v_g normalised when w == nullptr)
+__global__ void k_power_norm(const Dev D, double* v, const double* w, const double* nrm, const int* frozen) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= D.p; j += (int64_t)gridDim.x * blockDim.x) {
+    const int g = block_of_col(D, j);
+    if (frozen[g]) continue;
+    v[j] = (w ? w[j] : v[j]) / nrm[g];
+  }
+}
+
+// sample tau-quantile by exact rank selection and the null-model score psi/n (DESIGN reading R4)
+__global__ void k_null_score(const double* y, int n, const double* tau, int R, double* psi /*[R][n]*/) {
+  __shared__ double ys[2048];
+  __shared__ int cnt[3];
+  __shared__ double qsh;
+  for (int r = 0; r < R; ++r) {
+    int k = (int)ceil((double)n * tau[r]);
+    if (k < 1) k = 1;
+    if (k > n) k = n;
+    if (threadIdx.x == 0) {
+      cnt[0] = cnt[1] = cnt[2] = 0;
+      qsh = 0.0;
+    }
+    __syncthreads();
+    // rank_i = #{y_j < y_i} + #{j < i : y_j == y_i}; the element of rank k-1 is y_(k)
+    for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+      const int i = i0 + threadIdx.x;
+      const double yi = i < n ? y[i] : 0.0;
+      int rank = 0;
+      for (int t0 = 0; t0 < n; t0 += 2048) {
+        __syncthreads();
+        for (int t = threadIdx.x; t < 2048 && t0 + t < n; t += blockDim.x) ys[t] = y[t0 + t];
+        __syncthreads();
+        const int tn = min(2048, n - t0);
+        for (int t = 0; t < tn; ++t) {
+          const double yt = ys[t];
+          rank += (yt < yi) || (yt == yi && t0 + t < i);
+        }
+      }
+      if (i < n && rank == k - 1) qsh = yi;
+    }
+    __syncthreads();
+    const double q = qsh;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const double yi = y[i];
+      atomicAdd(&cnt[yi < q ? 0 : (yi > q ? 2 : 1)], 1);
+    }
+    __syncthreads();
+    const double t = tau[r];
+    const double tie = -((double)cnt[0] * (t - 1.0) + (double)cnt[2] * t) / (double)cnt[1];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const double yi = y[i];
+      psi[(int64_t)r * n + i] = (yi < q ? t - 1.0 : (yi > q ? t : tie)) / (double)n;
+    }
+    __syncthreads();
+  }
+}
+
+// support list of the current beta (parity par) — used after set_state
+__global__ void k_build_support(const Dev D, int par) {
+  const int lane = threadIdx.x & 31;
+  const double* beta = D.beta[par];
+  const int R = D.R;
+  for (int64_t c0 = (int64_t)blockIdx.x * blockDim.x; c0 < D.p; c0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = c0 + threadIdx.x;
+    bool nz = false;
+    double mx[FSQR_MAXR];
+    for (int r = 0; r < R; ++r) {
+      mx[r] = 0.0;
+      if (c < D.p && beta[(c + 1) * R + r] != 0.0) nz = true;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, nz);
+    if (m == 0) continue;
+    int base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd(D.sup_cnt + par, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    if (nz) {
+      const int e = base + __popc(m & ((1u << lane) - 1u));
+      D.sup_idx[par][e] = (int32_t)c;
+      for (int r = 0; r < R; ++r) {
+        const double b = beta[(c + 1) * R + r];
+        const double cv = b * D.inv_sd[c];
+        D.sup_c[par][(int64_t)e * R + r] = cv;
+        D.sup_b[par][(int64_t)e * R + r] = b;
+        if (cv != 0.0) atomicMax(D.cmax + par * R + r, (unsigned long long)__double_as_longlong(fabs(cv)));
+      }
+    }
+  }
+}
+
+// penalty of the committed beta and original-scale conversion (one CTA, fixed order)
+__global__ void __launch_bounds__(FT) k_commit_stats(const Dev D, double* pen_out /*[R]*/, double* beta_out /*[R][p+1] or null*/,
+                                                     int orig) {
+  __shared__ double smd[32 * 2 + 2];
+  const long long k = *D.iter;
+  for (int r = 0; r < D.R; ++r) {
+    const long long ci = D.status[r] == ST_ACTIVE ? k : D.commit_iter[r];
+    const double* beta = D.beta[(int)(ci & 1)];
+    double a[2] = {0.0, 0.0};
+    for (int64_t j = 1 + threadIdx.x; j <= D.p; j += blockDim.x) {
+      const double b = beta[j * D.R + r];
+      const double w = D.lamw ? D.lamw[j] : 1.0;
+      a[0] += D.lam_cur[r] * w * fabs(b);
+      const double bo = b * D.inv_sd[j - 1];
+      a[1] += D.mean[j - 1] * bo;
+      if (beta_out) beta_out[(int64_t)r * (D.p + 1) + j] = orig ? bo : b;
+    }
+    block_sum<2>(a, smd);
+    if (threadIdx.x == 0) {
+      if (pen_out) pen_out[r] = a[0];
+      if (beta_out) beta_out[(int64_t)r * (D.p + 1)] = orig ? beta[r] - a[1] : beta[r];
+    }
+    __syncthreads();
+  }
+}
+
+// resume after a solve froze some RHS: bring their committed beta into the current parity buffer
+__global__ void k_unfreeze(const Dev D) {
+  const long long k = *D.iter;
+  const int par = (int)(k & 1);
+  for (int r = 0; r < D.R; ++r) {
+    if (D.status[r] == ST_ACTIVE) continue;
+    const int cp = (int)(D.commit_iter[r] & 1);
+    if (cp == par) continue;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= D.p; j += (int64_t)gridDim.x * blockDim.x)
+      D.beta[par][j * D.R + r] = D.beta[cp][j * D.R + r];
+  }
+}
+
+}  // namespace
+
+void launch_finalize(const Dev& D, cudaStream_t st) { k_finalize<<<1, FT, 0, st>>>(D); }
+void launch_init_state(const Dev& D, cudaStream_t st) { k_init_state<<<1, FT, 0, st>>>(D); }
+void launch_colstats(const Dev& D, int32_t* colsum, double* mean, double* inv_sd, double* sd, int* bad,
+                     cudaStream_t st) {
+  const int grid = 148 * 8;
+  if (D.storage == 0) k_colstats_f32<<<grid, 256, 0, st>>>(D, mean, inv_sd, sd, bad);
+  else if (D.storage == 1) k_colstats_int<1><<<grid, 256, 0, st>>>(D, colsum, mean, inv_sd, sd, bad);
+  else k_colstats_int<2><<<grid, 256, 0, st>>>(D, colsum, mean, inv_sd, sd, bad);
+}
+void launch_power_start(int64_t p1, uint64_t seed, double* v, cudaStream_t st) {
+  k_power_start<<<256, 256, 0, st>>>(p1, seed, v);
+}
+void launch_power_fwd(const Dev& D, const int64_t* bstart, const double* v, const int* frozen, double* u,
+                      cudaStream_t st) {
+  dim3 grid((D.n + 127) / 128, D.G);
+  k_power_fwd<<<grid, 128, 0, st>>>(D, bstart, v, frozen, u);
+}
+void launch_back_f64(const Dev& D, const double* u, int per_block, const int* frozen, double* w,
+                     unsigned long long* maxbits, cudaStream_t st) {
+  k_back_f64<<<148 * 8, 256, 0, st>>>(D, u, per_block, frozen, w, maxbits);
+}
+void launch_power_reduce(const Dev& D, const int64_t* bstart, const double* v, const double* w, const int* frozen,
+                         double* est, double* nrm, cudaStream_t st) {
+  k_power_reduce<<<D.G, 1024, 0, st>>>(bstart, v, w, frozen, est, nrm);
+}
+void launch_power_norm(const Dev& D, double* v, const double* w, const double* nrm, const int* frozen,
+                       cudaStream_t st) {
+  k_power_norm<<<512, 256, 0, st>>>(D, v, w, nrm, frozen);
+}
+void launch_null_score(const double* y, int n, const double* tau, int R, double* psi, cudaStream_t st) {
+  k_null_score<<<1, 1024, 0, st>>>(y, n, tau, R, psi);
+}
+void launch_build_support(const Dev& D, int par, cudaStream_t st) {
+  k_build_support<<<(int)((D.p + 255) / 256 < 4096 ? (D.p + 255) / 256 : 4096), 256, 0, st>>>(D, par);
+}
+void launch_commit_stats(const Dev& D, double* pen, double* beta_out, int orig, cudaStream_t st) {
+  k_commit_stats<<<1, FT, 0, st>>>(D, pen, beta_out, orig);
+}
+void launch_unfreeze(const Dev& D, cudaStream_t st) { k_unfreeze<<<256, 256, 0, st>>>(D); }
