@@ -1,0 +1,309 @@
+#!/usr/bin/env python
+"""bench.py — FS-QRPPA hot path on B200: PPA iterations/s and X-streaming HBM GB/s.
+
+Workload (BASELINE.json metric): the C5 design and response (n=10k, p=1M uint8 genotypes,
+MAF ~ U(0.05, 0.5), skew-normal noise) with a single RHS tau=0.5, lambda = 0.02 lambda_max,
+G=48 ("m" in datagen.CONFIGS).  A step is one outer FS-QRPPA iteration (all SURVEY §8(a)
+rows a1-a6): one pass over X (10 GB) through the tcgen05 X~^T theta + beta-prox kernel, the
+support-gather forward product and the finalize kernel.  Before the warm-up the solver runs a
+200-iteration cold-start burn-in so the support is non-trivial.
+X (10 GB) is far larger than L2 (126 MB), so no L2 flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU: the path is single-GPU by north_star ("replicas only"); with N ranks
+each GPU runs an independent replica and value = total iterations / max time over ranks.
+--impl reference: the oracle (oracle/, plain fp64 C, all host cores) on a column sample of the
+same workload, reported in the same unit (iterations/s of the full problem).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import datagen  # noqa: E402
+
+METRIC = "PPA iters/sec and X-streaming HBM GB/s (% of peak) at n=10k, p=1M, tau=0.5"
+FALLBACK_HBM = 6650.0
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, idx: int, path: str):
+        self.path = path
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(idx), f"--query-gpu={q}", "--format=csv,noheader",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1].split()[0]))
+                mx = float(parts[2].split()[0])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def k2_traffic(name: str):
+    """dram bytes per K2 launch from the committed ncu --set full capture (profiles/), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(name)
+    except Exception:
+        return None
+
+
+def cpu_baseline(prob, lam_frac, tau, G, mu, budget_s=20.0):
+    """The oracle as it stands (plain fp64 C, OpenMP over all host cores) on a contiguous column
+    sample of the same workload; scaled to iterations/s of the full problem."""
+    import oracle
+
+    cores = os.cpu_count()
+    p_s = max(1000, min(prob.p, 60000))
+    X = prob.X[:p_s]
+    d = oracle.Design(prob.storage, prob.n, p_s, prob.ld, X)
+    lm, _ = oracle.lambda_max(d, prob.y, tau)
+    lam = oracle.lam_vector(p_s, lam_frac * lm)
+    st = oracle.blocks(p_s + 1, G)
+    eta = 1.05 * mu * (prob.n - 1) * np.diff(st).astype(np.float64)  # trace bound >= Lambda_max
+    t0 = time.perf_counter()
+    oracle.solve(d, prob.y, tau, lam, eta, mu, G, max_iter=1, check=False)
+    t1 = time.perf_counter()
+    k = max(1, min(50, int(budget_s / max(t1 - t0, 1e-3))))
+    t0 = time.perf_counter()
+    oracle.solve(d, prob.y, tau, lam, eta, mu, G, max_iter=k, check=False)
+    dt = time.perf_counter() - t0
+    frac = p_s / prob.p
+    return {"value": k * frac / dt, "unit": "iters/s", "cores": cores, "kind": "oracle",
+            "sample": f"{k} oracle iterations on columns 0..{p_s - 1} of {prob.p} ({frac:.4f} of X), "
+                      f"rate scaled by the column fraction; OMP threads = {cores}"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    prob = datagen.make(args.config)
+    tau = prob.taus[0]
+    G = prob.G
+    mu = 2.0 / prob.n
+    import oracle
+
+    cores = os.cpu_count()
+    # size the column sample so that warmup + steps fit in ~150 s of host time
+    p_probe = min(prob.p, 20000)
+    d = oracle.Design(prob.storage, prob.n, p_probe, prob.ld, prob.X[:p_probe])
+    lm, _ = oracle.lambda_max(d, prob.y, tau)
+    lam = oracle.lam_vector(p_probe, prob.lam_frac * lm)
+    eta = 1.05 * mu * (prob.n - 1) * np.diff(oracle.blocks(p_probe + 1, G)).astype(np.float64)
+    t0 = time.perf_counter()
+    oracle.solve(d, prob.y, tau, lam, eta, mu, G, max_iter=1, check=False)
+    per_col = (time.perf_counter() - t0) / p_probe
+    p_s = int(min(prob.p, max(1000, 150.0 / max(args.steps + args.warmup, 1) / per_col)))
+    d = oracle.Design(prob.storage, prob.n, p_s, prob.ld, prob.X[:p_s])
+    lm, _ = oracle.lambda_max(d, prob.y, tau)
+    lam = oracle.lam_vector(p_s, prob.lam_frac * lm)
+    eta = 1.05 * mu * (prob.n - 1) * np.diff(oracle.blocks(p_s + 1, G)).astype(np.float64)
+    w = oracle.solve(d, prob.y, tau, lam, eta, mu, G, max_iter=args.warmup, check=False)
+    st = (w["beta"], w["z"], w["theta"])
+    t0 = time.perf_counter()
+    oracle.solve(d, prob.y, tau, lam, eta, mu, G, max_iter=args.steps, check=False, state=st)
+    dt = time.perf_counter() - t0
+    frac = p_s / prob.p
+    value = args.steps * frac / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1000.0 / args.steps / frac,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C5 design/response, single RHS tau=0.5 (BASELINE metric)", "n": prob.n,
+                   "p": prob.p, "storage": "u8", "tau": tau, "lambda_frac": prob.lam_frac, "G": G,
+                   "column_sample": p_s},
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": cores, "kind": "oracle",
+                         "sample": f"each step = one oracle iteration on columns 0..{p_s - 1} ({frac:.4f} of X); "
+                                   f"rate scaled by the column fraction"},
+        "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2601_02826_b200 as fs
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    t_gen = time.perf_counter()
+    prob = datagen.make(args.config)
+    t_gen = time.perf_counter() - t_gen
+    tau = prob.taus[0]
+    G = prob.G
+    mu = 2.0 / prob.n
+    Xd = torch.from_numpy(prob.X).to(dev)
+    yd = torch.from_numpy(prob.y).to(dev)
+    torch.cuda.synchronize()
+
+    # setup (a0, a0', lambda_max) timed separately; lambda = frac * lambda_max from the GPU
+    t0 = time.perf_counter()
+    S = fs.Solver(Xd, prob.storage, prob.n, prob.p, prob.ld, yd, [tau], [1.0], G=G, mu=mu)
+    lm = float(S.lambda_max()[0])
+    S.set_lambda([prob.lam_frac * lm])
+    t_setup = time.perf_counter() - t0
+    eta = S.eta()
+
+    S.iterate(args.burn_in)
+    S.iterate(args.warmup)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(local, os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else ".",
+                                     f"clocks_rank{rank}.csv"))
+    stage_ms, total_ms = fs.fsqr_profile_iterate(S.ctx, args.steps)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    if ws > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    k = args.steps
+    value = k * ws / (total_ms / 1000.0)
+    nnz = int(S.trace(1)[-1, 0, 4]) if k > 0 else 0
+
+    # roofline of the dominant kernel (K2: X~^T theta + beta prox), algorithmic bytes per launch
+    xbytes = prob.n * prob.p                        # every stored genotype byte, read once
+    state_bytes = 28 * prob.p                       # beta r/w (16 B) + colsum (4 B) + 1/s_j (8 B) per column
+    k2_ms = stage_ms[0] / k
+    peak, peak_kind = peaks()
+    achieved = (xbytes + state_bytes) / (k2_ms / 1000.0) / 1e9
+    traffic = k2_traffic(args.config)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "kernel": f"k2_{S.backend}", "peak_source": peak_kind,
+            "algorithmic_bytes_per_launch": xbytes + state_bytes,
+            "kernel_share_of_step": stage_ms[0] / total_ms}
+
+    # e2e through the public C-ABI host-buffer entry (fsqr_fit_host): H2D copy of X and y from pinned
+    # memory, setup, k iterations and the D2H read of beta all inside the timed region.
+    e2e = None
+    if not args.no_e2e:
+        Xp = torch.empty(prob.X.shape, dtype=torch.uint8, pin_memory=True)
+        Xp.numpy()[:] = prob.X
+        yp = torch.empty(prob.n, dtype=torch.float64, pin_memory=True)
+        yp.numpy()[:] = prob.y
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        beta_h, _ = fs.fsqr_fit_host(Xp.numpy(), prob.storage, prob.n, prob.p, prob.ld, yp.numpy(), [tau],
+                                     [prob.lam_frac * lm], k, opt=fs.default_options(G=G, mu=mu), eta=eta)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        e2e = {"value": k / dt, "unit": "iters/s", "h2d_bytes_per_step": (prob.X.nbytes + prob.y.nbytes) / k,
+               "d2h_bytes_per_step": beta_h.nbytes / k,
+               "note": "one fsqr_fit_host call: H2D of X,y (pinned) + setup (eta given) + k iterations + D2H beta"}
+        del Xp
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cpu = cpu_baseline(prob, prob.lam_frac, tau, G, mu)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": ws, "steps": k, "warmup": args.warmup,
+            "ms_per_step": total_ms / k, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u8xs8->s32 exact, f64", "data": "synthetic",
+            "config": {"workload": "C5 design/response, single RHS tau=0.5 (BASELINE metric)", "n": prob.n,
+                       "p": prob.p, "storage": "u8", "tau": tau, "lambda": prob.lam_frac * lm, "lambda_frac":
+                       prob.lam_frac, "G": G, "mu": mu, "burn_in": args.burn_in, "support": nnz,
+                       "l2": "X (10 GB) >> L2 (126 MB): no flush needed", "parallelism": f"replicas x{ws}",
+                       "backend": S.backend, "setup_s": t_setup, "datagen_s": t_gen},
+            "x_stream_gbs": xbytes / (total_ms / k / 1000.0) / 1e9,
+            "x_stream_frac_of_peak": xbytes / (total_ms / k / 1000.0) / 1e9 / peak,
+            "stage_ms_per_step": {"k2_xt_theta_prox": stage_ms[0] / k, "k1_forward": stage_ms[1] / k,
+                                  "finalize": stage_ms[2] / k},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 3 * k,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="m")
+    ap.add_argument("--burn-in", dest="burn_in", type=int, default=200)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -177,6 +177,12 @@ fsqr_status fsqr_path_beta(fsqr_ctx* ctx, int32_t r, int32_t t, int64_t cap, int
  * for the last iterations, oldest first; returns rows written in *rows. */
 fsqr_status fsqr_trace(fsqr_ctx* ctx, double* out_host, int64_t cap_rows, int64_t* rows);
 
+/* Measurement entry: run exactly k iterations like fsqr_iterate but as individual launches with
+ * CUDA events around each stage on `stream`; returns the summed device time per stage
+ * stage_ms_host[3] = {X~^T theta + beta prox (a1,a2,a6), X~ beta (a4), finalize (a3,a5)} and
+ * the total (first to last event).  Blocking. */
+fsqr_status fsqr_profile_iterate(fsqr_ctx* ctx, int64_t k, double* stage_ms_host, double* total_ms_host, void* stream);
+
 /* total outer iterations since create/set_state (device counter; synchronises). */
 int64_t fsqr_iterations(fsqr_ctx* ctx);
 

@@ -380,6 +380,8 @@ int orc_solve(const orc_design* X, const double* y, const orc_opts* o, double* b
   int status = 2;
   int64_t k = 0;
   for (;; ++k) {
+    /* fixed-count mode: the state after max_iter updates is the output; its R is not needed */
+    if (!o->check && k == o->max_iter && k > 0 && !trace) { status = 2; break; }
     orc_backprod(X, theta, g);
     double Rk[3];
     kkt_parts(n, p1, y, o->tau, o->lam, beta, z, theta, g, s, Rk);

@@ -55,6 +55,7 @@ class fsqr_result(ctypes.Structure):
 EXPORTS = ["fsqr_default_options", "fsqr_create", "fsqr_iterate", "fsqr_solve", "fsqr_objective", "fsqr_kkt",
            "fsqr_get_beta", "fsqr_get_state", "fsqr_set_state", "fsqr_set_lambda", "fsqr_lambda_max",
            "fsqr_get_eta", "fsqr_get_colstats", "fsqr_path", "fsqr_path_beta", "fsqr_trace", "fsqr_iterations",
+           "fsqr_profile_iterate",
            "fsqr_backend_name", "fsqr_fit_host", "fsqr_last_error", "fsqr_global_error", "fsqr_status_str",
            "fsqr_destroy"]
 
@@ -97,6 +98,8 @@ def load(build_if_missing: bool = True):
     L.fsqr_path.argtypes = [ctxp, P, I32, P, P, P, P, P, P, P]
     L.fsqr_path_beta.argtypes = [ctxp, I32, I32, I64, P, P, P]
     L.fsqr_trace.argtypes = [ctxp, P, I64, P]
+    L.fsqr_profile_iterate.argtypes = [ctxp, I64, P, P, P]
+    L.fsqr_profile_iterate.restype = S
     L.fsqr_iterations.argtypes = [ctxp]
     L.fsqr_iterations.restype = I64
     L.fsqr_backend_name.argtypes = [ctxp]
@@ -273,6 +276,14 @@ def fsqr_trace(ctx, n_rhs: int, cap_rows: int) -> np.ndarray:
     rows = ctypes.c_int64(0)
     _check(load().fsqr_trace(ctx, _ptr(out), cap_rows, ctypes.byref(rows)), ctx)
     return out[: rows.value]
+
+
+def fsqr_profile_iterate(ctx, k: int, stream=None):
+    """k iterations as individual launches with CUDA events per stage: (stage_ms[3], total_ms)."""
+    st = np.zeros(3)
+    tot = ctypes.c_double(0.0)
+    _check(load().fsqr_profile_iterate(ctx, int(k), _ptr(st), ctypes.byref(tot), _stream(stream)), ctx)
+    return st, tot.value
 
 
 def fsqr_iterations(ctx) -> int:

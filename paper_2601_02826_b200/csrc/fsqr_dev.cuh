@@ -117,12 +117,14 @@ __device__ __forceinline__ double prox_rho1(double v, double tau) {
   return v > tau ? v - tau : (v < tau - 1.0 ? v + 1.0 - tau : 0.0);
 }
 
-// fixed-point exponent for the forward product: 2 n cnt max|c| 2^E < 2^61
+// fixed-point exponent for the forward product: 2 n cnt max|c| 2^E < 2^61 (no int64 overflow in
+// n*S - M) and max|c| 2^E < 2^43 (22-bit split of C in the int32 inner loop of k1)
 __device__ __forceinline__ int fwd_exponent(double cmax, long long cnt, int n) {
   if (!(cmax > 0.0) || cnt <= 0) return 0;
-  int e;
-  frexp(2.0 * (double)n * (double)cnt * cmax, &e);
-  return 61 - e;
+  int e1, e2;
+  frexp(2.0 * (double)n * (double)cnt * cmax, &e1);
+  frexp(cmax, &e2);
+  return min(61 - e1, 43 - e2);
 }
 
 __device__ __forceinline__ double warp_sum_d(double v) {
