@@ -101,6 +101,23 @@ def k2_traffic(name: str):
         return None
 
 
+def max_over_ranks(ms: float, device) -> float:
+    """Max of a per-rank device time over all ranks (the whole job ends with its slowest rank)."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return ms
+    t = torch.tensor([ms], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_value(steps: int, ws: int, max_ms: float) -> float:
+    """Weak scaling, replicas only: every rank runs `steps` iterations of its own replica."""
+    return steps * ws / (max_ms / 1000.0)
+
+
 def cpu_baseline(prob, lam_frac, tau, G, mu, budget_s=20.0):
     """The oracle as it stands (plain fp64 C, OpenMP over all host cores) on a contiguous column
     sample of the same workload; scaled to iterations/s of the full problem."""
@@ -217,13 +234,11 @@ def run_ours(args):
     stage_ms, total_ms = fs.fsqr_profile_iterate(S.ctx, args.steps)
     torch.cuda.synchronize()
     clocks = clk.stop()
+    total_ms = max_over_ranks(total_ms, dev)
     if ws > 1:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
         dist.barrier()
     k = args.steps
-    value = k * ws / (total_ms / 1000.0)
+    value = whole_job_value(k, ws, total_ms)
     nnz = int(S.trace(1)[-1, 0, 4]) if k > 0 else 0
 
     # roofline of the dominant kernel (K2: X~^T theta + beta prox), algorithmic bytes per launch

@@ -23,6 +23,7 @@
  *   2bit: X[c * ld + i/4] bits 2*(i%4)..2*(i%4)+1, ld = round_up(ceil(n/4), 16)
  *   f32:  X[c * ld + i], ld = round_up(n, 4) floats, pad = 0
  */
+#define _GNU_SOURCE
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -128,47 +129,61 @@ void dg_genotypes(uint64_t seed, int64_t n, int64_t p, const double* f, int pack
  * LD-structured genotypes (config 4): per individual, within blocks of `blk`
  * SNPs, a latent AR(1) L_j = rho L_{j-1} + sqrt(1-rho^2) xi_j (L_first ~ N(0,1))
  * thresholded at HWE quantiles so that P(G>=1) = 1-(1-f)^2, P(G=2) = f^2.
+ *
+ * Throughput matters here (C4 is 4e10 latent draws): individuals are taken in
+ * groups of four (one packed byte); for each SNP c the group's four innovations
+ * xi come from two 64-bit counter draws keyed by (c, group), each split into
+ * two 32-bit uniforms and turned into a pair of normals by both branches of
+ * Box-Muller in single precision (a DGP needs no more).  Both layouts use the
+ * same draws, so the u8 and 2-bit designs hold identical codes.
  */
+static inline void ld_normals4(uint64_t key, uint64_t ctr, float* xi) {
+  for (int h = 0; h < 2; ++h) {
+    uint64_t u = mix64(key ^ (2u * ctr + (uint64_t)h));
+    float u1 = ((float)(uint32_t)(u >> 40) + 0.5f) * 0x1.0p-24f;    /* (0,1), 24-bit */
+    float u2 = ((float)(uint32_t)(u & 0xFFFFFFu) + 0.5f) * 0x1.0p-24f;
+    float r = sqrtf(-2.0f * logf(u1));
+    float s, c;
+    sincosf(6.28318530717958647692f * u2, &s, &c);
+    xi[2 * h] = r * c;
+    xi[2 * h + 1] = r * s;
+  }
+}
+
 void dg_genotypes_ld(uint64_t seed, int64_t n, int64_t p, const double* f, double rho, int64_t blk,
                      int packed, int64_t ld, uint8_t* X) {
-  double* t1 = (double*)malloc(sizeof(double) * (size_t)p);
-  double* t2 = (double*)malloc(sizeof(double) * (size_t)p);
+  float* t1 = (float*)malloc(sizeof(float) * (size_t)p);
+  float* t2 = (float*)malloc(sizeof(float) * (size_t)p);
 #pragma omp parallel for schedule(static)
   for (int64_t c = 0; c < p; ++c) {
-    t1[c] = dg_probit((1.0 - f[c]) * (1.0 - f[c]));
-    t2[c] = dg_probit(1.0 - f[c] * f[c]);
+    t1[c] = (float)dg_probit((1.0 - f[c]) * (1.0 - f[c]));
+    t2[c] = (float)dg_probit(1.0 - f[c] * f[c]);
   }
-  const double sr = sqrt(1.0 - rho * rho);
-  int64_t nblk = (p + blk - 1) / blk;
-  if (packed) {
-    int64_t nb = (n + 3) / 4;
+  const float rf = (float)rho, sr = (float)sqrt(1.0 - rho * rho);
+  const uint64_t key = mix64(mix64(seed) ^ (STREAM_LATENT * 0xD1B54A32D192ED03ull));
+  const int64_t nblk = (p + blk - 1) / blk, nb = (n + 3) / 4;
 #pragma omp parallel for schedule(static)
-    for (int64_t c = 0; c < p; ++c) memset(X + c * ld, 0, (size_t)ld);
+  for (int64_t c = 0; c < p; ++c) memset(X + c * ld, 0, (size_t)ld);
+  /* work item = (SNP block b, run of 64 groups of four individuals) */
+  const int64_t RUN = 64, nrun = (nb + RUN - 1) / RUN;
 #pragma omp parallel for schedule(dynamic, 1)
-    for (int64_t q = 0; q < nblk * nb; ++q) {
-      int64_t b = q / nb, ib = q % nb;
-      int64_t c0 = b * blk, c1 = c0 + blk < p ? c0 + blk : p;
-      for (int64_t i = ib * 4; i < ib * 4 + 4 && i < n; ++i) {
-        double L = 0.0;
-        for (int64_t c = c0; c < c1; ++c) {
-          double xi = dg_normal(seed, STREAM_LATENT, (uint64_t)c * (uint64_t)n + (uint64_t)i);
-          L = (c == c0) ? xi : rho * L + sr * xi;
-          int g = (L > t1[c]) + (L > t2[c]);
-          X[c * ld + (i >> 2)] |= (uint8_t)(g << (2 * (i & 3)));
+  for (int64_t q = 0; q < nblk * nrun; ++q) {
+    const int64_t b = q / nrun, g0 = (q % nrun) * RUN, g1 = g0 + RUN < nb ? g0 + RUN : nb;
+    const int64_t c0 = b * blk, c1 = c0 + blk < p ? c0 + blk : p;
+    for (int64_t gi = g0; gi < g1; ++gi) {
+      float L[4] = {0, 0, 0, 0}, xi[4];
+      const int nv = (int)(n - 4 * gi < 4 ? n - 4 * gi : 4);
+      for (int64_t c = c0; c < c1; ++c) {
+        ld_normals4(key, (uint64_t)c * (uint64_t)nb + (uint64_t)gi, xi);
+        uint32_t byte = 0;
+        for (int s = 0; s < 4; ++s) {
+          L[s] = (c == c0) ? xi[s] : rf * L[s] + sr * xi[s];
+          uint32_t g = (uint32_t)(L[s] > t1[c]) + (uint32_t)(L[s] > t2[c]);
+          if (s >= nv) g = 0;
+          if (packed) byte |= g << (2 * s);
+          else X[c * ld + 4 * gi + s] = (uint8_t)g;
         }
-      }
-    }
-  } else {
-#pragma omp parallel for schedule(dynamic, 16)
-    for (int64_t i = 0; i < n; ++i) {
-      for (int64_t b = 0; b < nblk; ++b) {
-        int64_t c0 = b * blk, c1 = c0 + blk < p ? c0 + blk : p;
-        double L = 0.0;
-        for (int64_t c = c0; c < c1; ++c) {
-          double xi = dg_normal(seed, STREAM_LATENT, (uint64_t)c * (uint64_t)n + (uint64_t)i);
-          L = (c == c0) ? xi : rho * L + sr * xi;
-          X[c * ld + i] = (uint8_t)((L > t1[c]) + (L > t2[c]));
-        }
+        if (packed) X[c * ld + gi] = (uint8_t)byte;
       }
     }
   }

@@ -948,12 +948,19 @@ fsqr_status fsqr_fit_host(const fsqr_design* Xh, const double* y_host, int32_t n
   const size_t xb = (size_t)Xh->ld * (size_t)Xh->p * esz;
   void* dX = nullptr;
   double* dy = nullptr;
+  auto fail = [&](const char* what, cudaError_t e) {
+    if (dX) cudaFreeAsync(dX, st);
+    if (dy) cudaFreeAsync(dy, st);
+    return set_err(nullptr, e == cudaErrorMemoryAllocation ? FSQR_ERR_OOM : FSQR_ERR_CUDA, "%s: %s", what,
+                   cudaGetErrorString(e));
+  };
   cudaError_t e = cudaMallocAsync(&dX, xb, st);
-  if (e != cudaSuccess) return set_err(nullptr, FSQR_ERR_OOM, "device copy of X: %s", cudaGetErrorString(e));
+  if (e != cudaSuccess) return fail("device copy of X", e);
   e = cudaMallocAsync((void**)&dy, sizeof(double) * Xh->n, st);
-  if (e != cudaSuccess) return set_err(nullptr, FSQR_ERR_OOM, "device copy of y: %s", cudaGetErrorString(e));
-  cudaMemcpyAsync(dX, Xh->data_dev, xb, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(dy, y_host, sizeof(double) * Xh->n, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return fail("device copy of y", e);
+  e = cudaMemcpyAsync(dX, Xh->data_dev, xb, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dy, y_host, sizeof(double) * Xh->n, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return fail("host-to-device copy", e);
   fsqr_design Xd = *Xh;
   Xd.data_dev = dX;
   Xd.mean_dev = nullptr;

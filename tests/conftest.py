@@ -11,6 +11,7 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (run through gpurun)")
     config.addinivalue_line("markers", "slow: long-running")
+    config.addinivalue_line("markers", "fullsize: BASELINE.json full-size configs (GPU box, tens of GB host RAM)")
 
 
 @pytest.fixture(scope="session")

@@ -1,0 +1,127 @@
+"""GPU parity for the warm-started lambda path and the edge
+cases of the method: empty support (lambda >= lambda_max), a single column, the maximum RHS
+count (16 tau levels -> 64 digit rows of the tcgen05 B operand), ragged n, and p = 0 rejected.
+Every expected value comes from the fp64 oracle on the same seeded inputs."""
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+from gpu_helpers import make_pair, rel, to_device
+
+pytestmark = pytest.mark.gpu
+
+
+def test_path_matches_oracle(cuda_ok):
+    """C5 recipe at reduced size: 3 tau jointly on the GPU, a 6-point geometric grid from
+    lambda_max to 0.01 lambda_max with warm starts; per point the recorded iteration count,
+    objective and beta agree with the oracle's path for that tau."""
+    import paper_2601_02826_b200 as fs
+
+    prob = datagen.make("c5", n=500, p=1500)
+    d = oracle.Design.from_problem(prob)
+    taus = [0.1, 0.5, 0.9]
+    mu, G, T, tol = 2.0 / prob.n, 5, 6, 1e-5
+    eta = oracle.eta(d, G, mu)
+    lm = [oracle.lambda_max(d, prob.y, t)[0] for t in taus]
+    grid = np.array([[l * 0.01 ** (t / (T - 1)) for t in range(T)] for l in lm])
+    X, y = to_device(prob)
+    S = fs.Solver(X, prob.storage, prob.n, prob.p, prob.ld, y, taus, grid[:, 0], G=G, mu=mu, eta=eta, tol=tol,
+                  max_iter_point=4000)
+    res = S.path(grid)
+    for r, tau in enumerate(taus):
+        o = oracle.path(d, prob.y, tau, grid[r], eta, mu, G, tol, 4000)
+        assert np.all(np.abs(res["iters"][r] - o["iters"]) <= 2), (tau, res["iters"][r], o["iters"])
+        np.testing.assert_array_equal(res["converged"][r], o["converged"])
+        np.testing.assert_allclose(res["obj"][r], o["obj"], rtol=1e-4)
+        for t in range(T):
+            bg = S.path_beta(r, t)
+            bo = o["beta_path"][t]
+            assert rel(bg, bo) < 1e-4, (tau, t)
+            if abs(res["iters"][r][t] - o["iters"][t]) == 0:
+                assert np.array_equal(bg != 0, bo != 0), (tau, t)
+        # first point: lambda_max -> null model (beta_{1..p} = 0)
+        assert np.count_nonzero(S.path_beta(r, 0)[1:]) == 0
+
+
+def test_lambda_above_max_gives_null_model(cuda_ok):
+    """Empty support every iteration (K1 sees |S| = 0): beta_{1..p} = 0 and the intercept is the
+    sample tau-quantile (R4), as in the oracle."""
+    prob, d, S, cfg = make_pair("c2", n=900, p=700, taus=[0.3], lam_frac=1.0)
+    lam = 1.01 * cfg["lm"][0]
+    S.set_lambda([lam])
+    res = S.solve()
+    assert res["status"] == 0
+    b = S.beta()[0]
+    assert np.count_nonzero(b[1:]) == 0
+    q = np.sort(prob.y)[int(np.ceil(prob.n * 0.3)) - 1]
+    assert b[0] == pytest.approx(q, rel=1e-4, abs=1e-4)
+    o = oracle.solve(d, prob.y, 0.3, oracle.lam_vector(prob.p, lam), cfg["eta"], cfg["mu"], cfg["G"],
+                     max_iter=100000, tol=1e-6)
+    assert S.objective()[0] == pytest.approx(o["obj"], rel=1e-4)
+
+
+@pytest.mark.parametrize("storage", [0, 1, 2])
+def test_single_column_ragged_n(cuda_ok, storage):
+    """p = 1, n = 37 (not a multiple of 4, 16 or 128): the smallest admissible problem."""
+    name = "c1" if storage == 0 else "c2"
+    prob, d, S, cfg = make_pair(name, n=37, p=1, storage=storage, G=1, taus=[0.5], lam_frac=0.05)
+    S.iterate(100)
+    b, z, t = S.state()
+    o = oracle.solve(d, prob.y, 0.5, oracle.lam_vector(1, cfg["lams"][0]), cfg["eta"], cfg["mu"], 1, max_iter=100,
+                     check=False)
+    assert rel(b[0], o["beta"]) < 1e-6
+    assert rel(t[0], o["theta"]) < 1e-6
+
+
+def test_max_rhs_sixteen_tau(cuda_ok):
+    """R = 16 (FSQR_MAXR): 64 digit rows in the tcgen05 B operand; each RHS equals its oracle run."""
+    import paper_2601_02826_b200 as fs
+
+    prob = datagen.make("c2", n=640, p=900)
+    d = oracle.Design.from_problem(prob)
+    taus = list(np.linspace(0.05, 0.95, 16))
+    mu, G = 2.0 / prob.n, 5
+    eta = oracle.eta(d, G, mu)
+    lams = [0.05 * oracle.lambda_max(d, prob.y, t)[0] for t in taus]
+    X, y = to_device(prob)
+    S = fs.Solver(X, 1, prob.n, prob.p, prob.ld, y, taus, lams, G=G, mu=mu, eta=eta)
+    assert S.backend == "tc"
+    S.iterate(40)
+    b, z, t = S.state()
+    for r in (0, 7, 15):
+        o = oracle.solve(d, prob.y, taus[r], oracle.lam_vector(prob.p, lams[r]), eta, mu, G, max_iter=40, check=False)
+        assert rel(b[r], o["beta"]) < 1e-6, r
+        assert rel(t[r], o["theta"]) < 1e-6, r
+        assert np.array_equal(b[r] != 0, o["beta"] != 0), r
+
+
+def test_p_zero_and_too_many_rhs_rejected(cuda_ok):
+    import paper_2601_02826_b200 as fs
+
+    prob = datagen.make("c2", n=64, p=10)
+    X, y = to_device(prob)
+    with pytest.raises(fs.FsqrError) as e:
+        fs.Solver(X, 1, prob.n, 0, prob.ld, y, [0.5], [0.1], G=1)
+    assert e.value.status == -1
+    with pytest.raises(fs.FsqrError) as e:
+        fs.Solver(X, 1, prob.n, prob.p, prob.ld, y, [0.5] * 17, [0.1] * 17)
+    assert e.value.status == -1
+
+
+def test_converged_parity_c2_tau09(cuda_ok):
+    """C2 recipe (reduced) run to KKT tol 1e-6 at tau = 0.9: iteration count, objective, beta and
+    support agree with the oracle; the GPU point passes the oracle's fp64 certificate."""
+    prob, d, S, cfg = make_pair("c2", n=1200, p=4000, taus=[0.9], tol=1e-6, max_iter=200000)
+    res = S.solve()
+    assert res["status"] == 0, res
+    lv = oracle.lam_vector(prob.p, cfg["lams"][0])
+    o = oracle.solve(d, prob.y, 0.9, lv, cfg["eta"], cfg["mu"], cfg["G"], max_iter=200000, tol=1e-6)
+    assert o["status"] == 0
+    assert abs(res["iterations"] - o["iters"]) <= 2
+    b = S.beta()[0]
+    assert rel(b, o["beta"]) < 1e-4
+    assert S.objective()[0] == pytest.approx(o["obj"], rel=1e-4)
+    assert np.array_equal(b != 0, o["beta"] != 0)
+    _, z, t = S.state()
+    assert oracle.kkt_rel(d, prob.y, 0.9, lv, b, z[0], t[0]).max() < 2e-6
