@@ -62,10 +62,16 @@ typedef enum {
 } fsqr_storage;
 
 typedef enum {
-  FSQR_BACKEND_AUTO = 0,    /* tcgen05 for U8 (if supported shape), else SIMT */
-  FSQR_BACKEND_TC = 1,      /* tcgen05.mma kind::i8, TMA-staged tiles (U8 only) */
+  FSQR_BACKEND_AUTO = 0,    /* tcgen05 for U8 and PACKED2 (n_rhs <= 16), else SIMT */
+  FSQR_BACKEND_TC = 1,      /* tcgen05.mma kind::i8, TMA-staged tiles; PACKED2 unpacks into a TMEM A operand */
   FSQR_BACKEND_SIMT = 2     /* CUDA-core path (dp4a exact integer for U8/PACKED2, fp64 for F32) */
 } fsqr_backend;
+
+/* folded-concave penalties for the LLA driver (Section 5, Algorithm 2) */
+typedef enum {
+  FSQR_SCAD = 1,            /* p'_lambda of E16 (L354-361), a > 2 (a = 3.7 in the paper's studies, L404) */
+  FSQR_MCP = 2              /* p'_lambda of E17 (L363-369), a > 1 (a = 3 in the paper's studies, L404) */
+} fsqr_penalty;
 
 typedef struct {
   int32_t storage;          /* fsqr_storage */
@@ -85,7 +91,7 @@ typedef struct {
   double eta_safety;        /* eta_g = eta_safety * mu * Lambda_hat_g, default 1.05 */
   const double* eta_host;   /* optional [G]: use these eta_g instead of the power method */
   double tol;               /* stop when R(w^k) = max(R_p, R_beta, R_z) <= tol (reading R1) */
-  int64_t max_iter;         /* iteration cap for fsqr_solve */
+  int64_t max_iter;         /* iteration cap per fsqr_solve call (each LLA stage is one call) */
   int32_t power_max_iter;   /* power method cap (default 1000) */
   int32_t trace_cap;        /* rows of the per-iteration trace ring buffer (default 4096) */
   double power_tol;         /* power method relative tolerance (default 1e-4) */
@@ -112,8 +118,9 @@ void fsqr_default_options(fsqr_options* opt);
 /*
  * Create a solver for n_rhs (1..16) independent quantile levels sharing X.
  * y_dev: [n] response (copied).  tau_host, lambda_host: [n_rhs] (copied);
- * lambda_w_dev: optional [p+1] non-negative penalty weights w_j (lam_j = lambda * w_j,
- * w_0 is ignored: the intercept is never penalised), NULL = all ones.
+ * lambda_w_dev: optional [p+1] non-negative penalty weights w_j (lam_j = lambda * w_j, the weighted
+ * l1 of E4, L150-155; copied and applied to every RHS; w_0 is ignored: the intercept is never
+ * penalised), NULL = all ones.
  * Performs a0 (column statistics, exact integer sums for genotype storage),
  * a0' (eta_g by the power method unless opt->eta_host) and lambda_max (per tau);
  * cold start beta = 0, z = y, theta = 0.  Synchronises `stream`.
@@ -125,7 +132,7 @@ fsqr_status fsqr_create(const fsqr_design* X, const double* y_dev, int32_t n_rhs
 /* Enqueue exactly k outer iterations (a1-a5), ignoring the stopping test.  Asynchronous. */
 fsqr_status fsqr_iterate(fsqr_ctx* ctx, int64_t k, void* stream);
 
-/* Iterate until every RHS satisfies R(w^k) <= tol or max_iter total iterations (blocking).
+/* Iterate until every RHS satisfies R(w^k) <= tol or max_iter iterations of this call (blocking).
  * The committed iterate is the first w^k that passed (or the last one).  out may be NULL. */
 fsqr_status fsqr_solve(fsqr_ctx* ctx, fsqr_result* out, void* stream);
 
@@ -135,6 +142,27 @@ fsqr_status fsqr_objective(fsqr_ctx* ctx, double* obj_host, void* stream);
 
 /* Relative KKT residuals [n_rhs][3] = (R_p, R_beta, R_z) at the committed iterate; one pass over X. Blocking. */
 fsqr_status fsqr_kkt(fsqr_ctx* ctx, double* R_host, void* stream);
+
+/* HBIC (E18) per RHS at the committed iterate:
+ * log(sum_i rho_tau(y_i - x~_i^T beta)) + |A| (log log n / n) log p, |A| = #{j >= 1: beta_j != 0}.
+ * Uses the cached s = X~beta (no pass over X).  Blocking. */
+fsqr_status fsqr_hbic(fsqr_ctx* ctx, double* hbic_host, void* stream);
+
+/* Per-RHS penalty weights (weighted l1, E4 L150-155): w_host [n_rhs][p+1], lam_jr = lambda_r * w_jr,
+ * w >= 0 and finite (else FSQR_ERR_CONFIG), w_0 ignored; NULL restores unit weights.  The state is
+ * kept (warm start).  Blocking. */
+fsqr_status fsqr_set_lambda_weights(fsqr_ctx* ctx, const double* w_host, void* stream);
+
+/*
+ * L-step LLA for SCAD or MCP (Algorithm 2): solve with the current weights
+ * (unit weights = the LASSO stage), then L times set lam_j = p'_lambda(|beta~_j|) from the committed
+ * solution (device kernel, E16/E17) and solve again warm-started from (beta~, z~, theta~).  Each
+ * stage runs to tol / max_iter as fsqr_solve.  stage_iters_host [L+1] (may be NULL) receives the
+ * iterations of each stage; out (may be NULL) the result of the last stage.  Blocking.
+ * Errors: FSQR_ERR_CONFIG for an unknown penalty, a out of range, L < 0 or lambda = 0.
+ */
+fsqr_status fsqr_lla(fsqr_ctx* ctx, int32_t penalty, double a, int32_t L, int64_t* stage_iters_host,
+                     fsqr_result* out, void* stream);
 
 /* beta of the committed iterate, [n_rhs][p+1] row per RHS.
  * scale 0: standardised; scale 1: original scale, beta_j/s_j and beta_0 - sum m_j beta_j/s_j (L404). */

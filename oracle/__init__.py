@@ -17,6 +17,10 @@ Parity status per function (DESIGN.md §4 repeats this table):
   lambda_max      pinned: textbook null model (beta=0, intercept = sample quantile) just above it
   solve           pinned: LP vertex enumeration + HiGHS (tiny), Prop. 1 certificate, partition
                   invariance, fixed-point property, geometric decay (Corollary 1)
+  penalty_deriv   pinned: SPEC worked values (SCAD, MCP), continuity at the knots, the LASSO limit
+  lla             pinned: each stage is a weighted-l1 PQR whose optimum matches the LP brute force
+                  with the stage's weights; Prop. 1 certificate per stage
+  hbic            pinned: SPEC worked value and the closed form on a null model
   trajectory after k iterations: parity unpinned beyond the composition of pinned steps
                   (the paper prints no iterates); see DESIGN.md §4.
 """
@@ -90,6 +94,13 @@ def _load():
         lib.orc_lambda_max.argtypes = [DP, P, D, P]
         lib.orc_solve.restype = ctypes.c_int
         lib.orc_solve.argtypes = [DP, P, ctypes.POINTER(_Opts), P, P, P, P, P, P, P]
+        lib.orc_penalty_deriv.restype = D
+        lib.orc_penalty_deriv.argtypes = [I32, D, D, D]
+        lib.orc_lla_weights.argtypes = [I32, D, D, P, I64, P]
+        lib.orc_hbic_value.restype = D
+        lib.orc_hbic_value.argtypes = [D, I64, I64, I64]
+        lib.orc_hbic.restype = D
+        lib.orc_hbic.argtypes = [DP, P, D, P]
         lib.orc_path.restype = I64
         lib.orc_path.argtypes = [DP, P, D, D, I32, P, P, P, I32, D, I64, P, P, P, P, P, P, P, P]
         _lib = lib
@@ -275,3 +286,46 @@ def path(d: Design, y, tau: float, lam_path, eta_vec, mu: float, G: int, tol: fl
                              _p(conv))
     return dict(total=int(total), iters=iters, R=R, obj=obj, converged=conv.astype(bool), beta_path=bp,
                 beta=beta, z=z, theta=theta)
+
+
+SCAD, MCP = 1, 2
+
+
+def penalty_deriv(kind: int, a: float, lam: float, b: float) -> float:
+    """p'_lambda(|b|): SCAD (E16, L354-361) or MCP (E17, L363-369)."""
+    return _load().orc_penalty_deriv(int(kind), float(a), float(lam), float(b))
+
+
+def lla_weights(kind: int, a: float, lam: float, beta) -> np.ndarray:
+    """w_j = p'_lambda(|beta_j|)/lambda for j >= 1, w_0 = 0 (Algorithm 2)."""
+    beta = _f64(beta)
+    w = np.empty_like(beta)
+    _load().orc_lla_weights(int(kind), float(a), float(lam), _p(beta), len(beta), _p(w))
+    return w
+
+
+def lla(d: Design, y, tau: float, lam: float, kind: int, a: float, L: int, eta_vec, mu: float, G: int,
+        tol: float = 1e-6, max_iter: int = 100000) -> dict:
+    """Algorithm 2: the LASSO fit with lambda_j = lambda, then L reweighted
+    l1 fits, each warm-started from the previous (beta~, z~, theta~) with
+    lambda~_j = p'_lambda(|beta~_j|)."""
+    stages = []
+    w = np.ones(d.p + 1)
+    w[0] = 0.0
+    state = None
+    for l in range(L + 1):
+        out = solve(d, y, tau, lam_vector(d.p, lam, w), eta_vec, mu, G, max_iter=max_iter, tol=tol, state=state)
+        stages.append(dict(weights=w.copy(), beta=out["beta"].copy(), iters=out["iters"], obj=out["obj"],
+                           status=out["status"]))
+        state = (out["beta"], out["z"], out["theta"])
+        w = lla_weights(kind, a, lam, out["beta"])
+    return dict(stages=stages, beta=stages[-1]["beta"], z=state[1], theta=state[2])
+
+
+def hbic_value(loss: float, active: int, n: int, p: int) -> float:
+    return _load().orc_hbic_value(float(loss), int(active), int(n), int(p))
+
+
+def hbic(d: Design, y, tau: float, beta) -> float:
+    """HBIC (E18, L408-411) with C_n = log p."""
+    return _load().orc_hbic(d.ref, _p(_f64(y)), float(tau), _p(_f64(beta)))

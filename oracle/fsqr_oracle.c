@@ -496,3 +496,50 @@ int64_t orc_path(const orc_design* X, const double* y, double tau, double mu, in
   free(r);
   return k;
 }
+
+/* ------------------------------------------------ folded-concave penalties (Section 5) */
+
+/*
+ * p'_lambda(|b|) for SCAD (kind 1, a > 2; E16) and MCP
+ * (kind 2, a > 1; E17), written exactly as displayed.
+ */
+double orc_penalty_deriv(int32_t kind, double a, double lam, double b) {
+  const double ab = fabs(b);
+  if (kind == 1) {
+    if (ab <= lam) return lam;
+    if (ab < a * lam) return (a * lam - ab) / (a - 1.0);
+    return 0.0;
+  }
+  if (ab <= a * lam) return lam - ab / a;
+  return 0.0;
+}
+
+/*
+ * LLA weights of Algorithm 2: lambda~_j = p'_lambda(|beta~_j|) for the
+ * penalised coefficients j >= 1, written as the weight w_j = p'_lambda(|beta~_j|) / lambda so
+ * that lambda_j = lambda * w_j (the weighted l1 of E4, L150-155); w_0 = 0 (intercept, L155).
+ */
+void orc_lla_weights(int32_t kind, double a, double lam, const double* beta, int64_t p1, double* w) {
+  w[0] = 0.0;
+  for (int64_t j = 1; j < p1; ++j) w[j] = orc_penalty_deriv(kind, a, lam, beta[j]) / lam;
+}
+
+/*
+ * HBIC (E18): log(sum_i rho_tau(y_i - x~_i^T beta)) + |A| (log log n / n) C_n
+ * with C_n = log p (L411).  |A| counts the nonzero penalised coefficients.
+ */
+double orc_hbic_value(double loss, int64_t active, int64_t n, int64_t p) {
+  return log(loss) + (double)active * (log(log((double)n)) / (double)n) * log((double)p);
+}
+
+double orc_hbic(const orc_design* X, const double* y, double tau, const double* beta) {
+  const int64_t n = X->n, p1 = X->p + 1;
+  double* s = (double*)malloc(sizeof(double) * n);
+  orc_fwdprod(X, beta, s);
+  double loss = 0.0;
+  for (int64_t i = 0; i < n; ++i) loss += orc_rho(y[i] - s[i], tau);
+  int64_t act = 0;
+  for (int64_t j = 1; j < p1; ++j) act += beta[j] != 0.0;
+  free(s);
+  return orc_hbic_value(loss, act, n, X->p);
+}

@@ -22,6 +22,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _lib = None
 
 F32_DENSE, U8, PACKED2 = 0, 1, 2
+SCAD, MCP = 1, 2
 BACKEND_AUTO, BACKEND_TC, BACKEND_SIMT = 0, 1, 2
 STATUS = {0: "FSQR_OK", 2: "FSQR_NOT_CONVERGED", -1: "FSQR_ERR_CONFIG", -2: "FSQR_ERR_DATA",
           -3: "FSQR_ERR_NUMERIC", -4: "FSQR_ERR_CUDA", -5: "FSQR_ERR_OOM", -6: "FSQR_ERR_STATE"}
@@ -55,7 +56,7 @@ class fsqr_result(ctypes.Structure):
 EXPORTS = ["fsqr_default_options", "fsqr_create", "fsqr_iterate", "fsqr_solve", "fsqr_objective", "fsqr_kkt",
            "fsqr_get_beta", "fsqr_get_state", "fsqr_set_state", "fsqr_set_lambda", "fsqr_lambda_max",
            "fsqr_get_eta", "fsqr_get_colstats", "fsqr_path", "fsqr_path_beta", "fsqr_trace", "fsqr_iterations",
-           "fsqr_profile_iterate",
+           "fsqr_profile_iterate", "fsqr_hbic", "fsqr_set_lambda_weights", "fsqr_lla",
            "fsqr_backend_name", "fsqr_fit_host", "fsqr_last_error", "fsqr_global_error", "fsqr_status_str",
            "fsqr_destroy"]
 
@@ -100,6 +101,9 @@ def load(build_if_missing: bool = True):
     L.fsqr_trace.argtypes = [ctxp, P, I64, P]
     L.fsqr_profile_iterate.argtypes = [ctxp, I64, P, P, P]
     L.fsqr_profile_iterate.restype = S
+    L.fsqr_hbic.argtypes = [ctxp, P, P]
+    L.fsqr_set_lambda_weights.argtypes = [ctxp, P, P]
+    L.fsqr_lla.argtypes = [ctxp, I32, D, I32, P, ctypes.POINTER(fsqr_result), P]
     L.fsqr_iterations.argtypes = [ctxp]
     L.fsqr_iterations.restype = I64
     L.fsqr_backend_name.argtypes = [ctxp]
@@ -116,7 +120,8 @@ def load(build_if_missing: bool = True):
     L.fsqr_destroy.restype = None
     for name in ("fsqr_create", "fsqr_iterate", "fsqr_solve", "fsqr_objective", "fsqr_kkt", "fsqr_get_beta",
                  "fsqr_get_state", "fsqr_set_state", "fsqr_set_lambda", "fsqr_lambda_max", "fsqr_get_eta",
-                 "fsqr_get_colstats", "fsqr_path", "fsqr_path_beta", "fsqr_trace", "fsqr_fit_host"):
+                 "fsqr_get_colstats", "fsqr_path", "fsqr_path_beta", "fsqr_trace", "fsqr_fit_host", "fsqr_hbic",
+                 "fsqr_set_lambda_weights", "fsqr_lla"):
         getattr(L, name).restype = S
     _lib = L
     return L
@@ -286,6 +291,28 @@ def fsqr_profile_iterate(ctx, k: int, stream=None):
     return st, tot.value
 
 
+def fsqr_hbic(ctx, n_rhs: int, stream=None) -> np.ndarray:
+    out = np.empty(n_rhs)
+    _check(load().fsqr_hbic(ctx, _ptr(out), _stream(stream)), ctx)
+    return out
+
+
+def fsqr_set_lambda_weights(ctx, weights=None, stream=None):
+    """weights: [n_rhs, p+1] (or None for unit weights)."""
+    w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
+    return _check(load().fsqr_set_lambda_weights(ctx, _ptr(w), _stream(stream)), ctx)
+
+
+def fsqr_lla(ctx, penalty: int, a: float, L: int, stream=None) -> dict:
+    it = np.zeros(L + 1, dtype=np.int64)
+    r = fsqr_result()
+    st = _check(load().fsqr_lla(ctx, int(penalty), float(a), int(L), _ptr(it), ctypes.byref(r), _stream(stream)), ctx)
+    R = r.n_rhs
+    return dict(status=st, stage_iters=it, rhs_status=[r.status[i] for i in range(R)],
+                R=np.array([[r.R[i][q] for q in range(3)] for i in range(R)]),
+                objective=np.array([r.objective[i] for i in range(R)]))
+
+
 def fsqr_iterations(ctx) -> int:
     return int(load().fsqr_iterations(ctx))
 
@@ -380,6 +407,15 @@ class Solver:
 
     def path_beta(self, r: int, t: int):
         return fsqr_path_beta(self.ctx, r, t, self.p)
+
+    def hbic(self):
+        return fsqr_hbic(self.ctx, self.R)
+
+    def set_lambda_weights(self, weights=None):
+        return fsqr_set_lambda_weights(self.ctx, weights)
+
+    def lla(self, penalty: int, a: float, L: int = 1):
+        return fsqr_lla(self.ctx, penalty, a, L)
 
     def trace(self, rows: int = 4096):
         return fsqr_trace(self.ctx, self.R, rows)

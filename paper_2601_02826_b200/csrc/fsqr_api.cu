@@ -37,6 +37,7 @@ void launch_null_score(const double* y, int n, const double* tau, int R, double*
 void launch_build_support(const Dev& D, int par, cudaStream_t st);
 void launch_commit_stats(const Dev& D, double* pen, double* beta_out, int orig, cudaStream_t st);
 void launch_unfreeze(const Dev& D, cudaStream_t st);
+void launch_lla_weights(const Dev& D, int kind, double a, cudaStream_t st);
 void launch_k1_mode(const Dev& D, int grid, cudaStream_t st, int cur);
 
 namespace {
@@ -58,7 +59,7 @@ struct fsqr_ctx {
   Graph graph[M_COUNT];
   int backend = FSQR_BACKEND_SIMT;
   int sms = 148;
-  int k2_grid = 148, k1_grid = 592;
+  int k2_grid = 148, k1_grid = 148;
   int chunk = 16;
   CUtensorMap tmX{}, tmB{};
   cudaStream_t cap_stream = nullptr;
@@ -126,7 +127,8 @@ fsqr_status make_tmaps(fsqr_ctx* ctx) {
   EncodeTiledFn enc = (EncodeTiledFn)fn;
   const Dev& D = ctx->D;
   {
-    cuuint64_t dims[2] = {(cuuint64_t)D.n, (cuuint64_t)D.p};
+    // u8: inner extent n samples; 2-bit: the packed column (ld bytes, zero padding beyond n/4)
+    cuuint64_t dims[2] = {(cuuint64_t)(D.storage == 2 ? D.ld : D.n), (cuuint64_t)D.p};
     cuuint64_t strides[1] = {(cuuint64_t)D.ld};
     cuuint32_t box[2] = {128, 128};
     cuuint32_t es[2] = {1, 1};
@@ -143,7 +145,7 @@ fsqr_status make_tmaps(fsqr_ctx* ctx) {
   {
     cuuint64_t dims[2] = {(cuuint64_t)D.ldk, (cuuint64_t)D.npad};
     cuuint64_t strides[1] = {(cuuint64_t)D.ldk};
-    cuuint32_t box[2] = {128, (cuuint32_t)D.npad};
+    cuuint32_t box[2] = {128, (cuuint32_t)(4 * D.R)};   // only the 4R live digit rows (rows up to npad stay 0 in smem)
     cuuint32_t es[2] = {1, 1};
     CUresult r = enc(&ctx->tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)D.Bq, dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -154,7 +156,9 @@ fsqr_status make_tmaps(fsqr_ctx* ctx) {
 }
 
 void launch_k2(fsqr_ctx* ctx, const Dev& D, cudaStream_t st) {
-  if (ctx->backend == FSQR_BACKEND_TC)
+  if (ctx->backend == FSQR_BACKEND_TC && D.storage == FSQR_PACKED2)
+    launch_k2_tc2(D, &ctx->tmX, &ctx->tmB, ctx->k2_grid, st);
+  else if (ctx->backend == FSQR_BACKEND_TC)
     launch_k2_tc(D, &ctx->tmX, &ctx->tmB, ctx->k2_grid, st);
   else
     launch_k2_simt(D, ctx->k2_grid, st);
@@ -417,16 +421,24 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
 
   // backend
   ctx->backend = FSQR_BACKEND_SIMT;
-  if (X->storage == FSQR_U8 && k2_tc_supported(D.npad) && o.backend != FSQR_BACKEND_SIMT) ctx->backend = FSQR_BACKEND_TC;
+  if (X->storage != FSQR_F32_DENSE && k2_tc_supported(D.npad) && o.backend != FSQR_BACKEND_SIMT)
+    ctx->backend = FSQR_BACKEND_TC;
   if (o.backend == FSQR_BACKEND_TC && ctx->backend != FSQR_BACKEND_TC)
-    return set_err(ctx, FSQR_ERR_CONFIG, "tcgen05 backend needs U8 storage and n_rhs <= 16");
+    return set_err(ctx, FSQR_ERR_CONFIG, "tcgen05 backend needs U8 or PACKED2 storage and n_rhs <= 16");
+  if (ctx->backend == FSQR_BACKEND_TC && X->storage == FSQR_PACKED2) {
+    // 2-bit tensor-core kernel: 512-sample K blocks, theta digits in its K order
+    D.ldk = (int)(((X->n + 511) / 512) * 512);
+    D.bperm = 1;
+  }
   if (ctx->backend == FSQR_BACKEND_TC) {
     CK(k2_tc_init());
+    CK(k2_tc2_init());
     ctx->k2_grid = (int)std::min<int64_t>((X->p + 127) / 128, ctx->sms);
   } else {
     ctx->k2_grid = ctx->sms * 8;
   }
-  ctx->k1_grid = ctx->sms * 4;
+  ctx->k1_grid = ctx->sms;   // k1_bulk scales by its resident CTAs per SM
+  CK(k1_init());
 
   // ---------------- allocations
   int32_t* colsum;
@@ -446,7 +458,17 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
   D.y = y;
   D.tau = tau_d;
   D.lam_cur = lam_cur;
-  D.lamw = lamw_dev;
+  // penalty weights: ctx-owned [(p+1)][R]; the caller's [p+1] vector (if any) is broadcast to every RHS
+  AL(D.lamw, p1 * R);
+  AL(D.use_w, 1);
+  if (lamw_dev) {
+    for (int r = 0; r < R; ++r)
+      CK(cudaMemcpy2DAsync(D.lamw + r, sizeof(double) * R, lamw_dev, sizeof(double), sizeof(double), p1,
+                           cudaMemcpyDeviceToDevice, st));
+    const int one = 1;
+    CK(cudaMemcpyAsync(D.use_w, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
   CK(cudaMemcpyAsync(y, y_dev, sizeof(double) * X->n, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(tau_d, tau, sizeof(double) * R, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(lam_cur, lambda, sizeof(double) * R, cudaMemcpyHostToDevice, st));
@@ -472,6 +494,10 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
   AL(D.mterm, R);
   AL(D.k2part, (size_t)std::max(ctx->k2_grid, ctx->sms * 8) * R * FSQR_NPART);
   AL(D.ticket, 1);
+  AL(D.kbase, 1);
+  AL(D.fpart, (size_t)FIN_MAXGRID * R * FSQR_FPART);
+  AL(D.ftsum, (size_t)FIN_MAXGRID * R);
+  AL(D.fticket, 1);
   AL(D.scal, R * FSQR_NSCAL);
   AL(D.status, R);
   AL(D.commit_iter, R);
@@ -675,7 +701,7 @@ fsqr_status fsqr_objective(fsqr_ctx* ctx, double* obj_host, void* stream) {
   if (!ctx || !obj_host) return set_err(ctx, FSQR_ERR_CONFIG, "null argument");
   cudaStream_t st = (cudaStream_t)stream;
   double* pen = nullptr;
-  CK(cudaMallocAsync(&pen, sizeof(double) * ctx->R, st));
+  CK(cudaMallocAsync(&pen, sizeof(double) * 2 * ctx->R, st));
   launch_commit_stats(ctx->D, pen, nullptr, 0, st);
   CK(cudaGetLastError());
   std::vector<double> hp(ctx->R), sc((size_t)ctx->R * FSQR_NSCAL);
@@ -685,6 +711,75 @@ fsqr_status fsqr_objective(fsqr_ctx* ctx, double* obj_host, void* stream) {
   CK(cudaStreamSynchronize(st));
   for (int r = 0; r < ctx->R; ++r) obj_host[r] = sc[r * FSQR_NSCAL + 2] / (double)ctx->n + hp[r];
   return FSQR_OK;
+}
+
+fsqr_status fsqr_hbic(fsqr_ctx* ctx, double* hbic_host, void* stream) {
+  if (!ctx || !hbic_host) return set_err(ctx, FSQR_ERR_CONFIG, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  double* pen = nullptr;
+  CK(cudaMallocAsync(&pen, sizeof(double) * 2 * ctx->R, st));
+  launch_commit_stats(ctx->D, pen, nullptr, 0, st);
+  CK(cudaGetLastError());
+  std::vector<double> hp(2 * ctx->R), sc((size_t)ctx->R * FSQR_NSCAL);
+  CK(cudaMemcpyAsync(hp.data(), pen, sizeof(double) * 2 * ctx->R, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(sc.data(), ctx->D.scal, sizeof(double) * sc.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaFreeAsync(pen, st));
+  CK(cudaStreamSynchronize(st));
+  const double n = (double)ctx->n, p = (double)ctx->p;
+  for (int r = 0; r < ctx->R; ++r)
+    hbic_host[r] = std::log(sc[r * FSQR_NSCAL + 2]) + hp[ctx->R + r] * (std::log(std::log(n)) / n) * std::log(p);
+  return FSQR_OK;
+}
+
+fsqr_status fsqr_set_lambda_weights(fsqr_ctx* ctx, const double* w_host, void* stream) {
+  if (!ctx) return set_err(nullptr, FSQR_ERR_CONFIG, "ctx is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int R = ctx->R;
+  const int64_t p1 = ctx->p + 1;
+  int flag = 0;
+  if (w_host) {
+    std::vector<double> t((size_t)p1 * R);
+    for (int r = 0; r < R; ++r)
+      for (int64_t j = 0; j < p1; ++j) {
+        const double w = w_host[(size_t)r * p1 + j];
+        if (!(w >= 0.0) || !std::isfinite(w))
+          return set_err(ctx, FSQR_ERR_CONFIG, "weight[%d][%lld]=%g invalid", r, (long long)j, w);
+        t[(size_t)j * R + r] = w;
+      }
+    CK(cudaMemcpyAsync(ctx->D.lamw, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice, st));
+    flag = 1;
+  }
+  CK(cudaMemcpyAsync(ctx->D.use_w, &flag, sizeof(int), cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  return FSQR_OK;
+}
+
+fsqr_status fsqr_lla(fsqr_ctx* ctx, int32_t penalty, double a, int32_t L, int64_t* stage_iters_host,
+                     fsqr_result* out, void* stream) {
+  if (!ctx) return set_err(nullptr, FSQR_ERR_CONFIG, "ctx is NULL");
+  if (penalty != FSQR_SCAD && penalty != FSQR_MCP) return set_err(ctx, FSQR_ERR_CONFIG, "penalty %d unknown", penalty);
+  if (penalty == FSQR_SCAD && !(a > 2.0)) return set_err(ctx, FSQR_ERR_CONFIG, "SCAD needs a > 2 (E16)");
+  if (penalty == FSQR_MCP && !(a > 1.0)) return set_err(ctx, FSQR_ERR_CONFIG, "MCP needs a > 1 (E17)");
+  if (L < 0) return set_err(ctx, FSQR_ERR_CONFIG, "L must be >= 0");
+  for (int r = 0; r < ctx->R; ++r)
+    if (!(ctx->lambda[r] > 0.0)) return set_err(ctx, FSQR_ERR_CONFIG, "LLA needs lambda > 0 (rhs %d)", r);
+  cudaStream_t st = (cudaStream_t)stream;
+  fsqr_result res{};
+  fsqr_status last = FSQR_OK;
+  for (int l = 0; l <= L; ++l) {
+    if (l > 0) {
+      // lambda~_j = p'_lambda(|beta~_j^{l-1}|) from the committed stage-(l-1) solution
+      launch_lla_weights(ctx->D, penalty, a, st);
+      CK(cudaGetLastError());
+      const int one = 1;
+      CK(cudaMemcpyAsync(ctx->D.use_w, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+    }
+    last = fsqr_solve(ctx, &res, stream);
+    if (last < 0) return last;
+    if (stage_iters_host) stage_iters_host[l] = res.iterations;
+  }
+  if (out) *out = res;
+  return last;
 }
 
 fsqr_status fsqr_kkt(fsqr_ctx* ctx, double* R_host, void* stream) {

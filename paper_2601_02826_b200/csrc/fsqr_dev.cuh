@@ -21,6 +21,9 @@
 #define FSQR_NSCAL 4          // per-RHS scalars of the current iterate: Rp, Rz, loss_sum, (spare)
 #define FSQR_MAXR 16
 #define FSQR_TRACE_W 5        // trace row: Rp, Rb, Rz, obj, nnz
+#define FSQR_FPART 8          // finalize partials per CTA and RHS: 7 sums + max|theta|
+#define FIN_THREADS 256
+#define FIN_MAXGRID 256       // ceil(65536 / FIN_THREADS)
 #define FSQR_PATH_W 7         // path record: iters, Rp, Rb, Rz, obj, nnz, converged
 
 enum { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_NUMERIC = 3 };
@@ -28,6 +31,7 @@ enum { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_NUMERIC = 3 };
 struct Dev {
   // sizes / layout
   int n, R, G, storage, npad, ldk;
+  int bperm;                        // 1: theta digit rows in the 2-bit tcgen05 K order (k2_tc2.cu)
   int64_t p, ld;
   int64_t gq, grem;                 // block partition of the p+1 model columns: q = (p+1)/G, rem
   // design (borrowed) + statistics
@@ -36,7 +40,8 @@ struct Dev {
   const int32_t* colsum;            // exact integer column sums (genotype storage)
   const double* mean;
   const double* inv_sd;
-  const double* lamw;               // [p+1] or nullptr
+  double* lamw;                     // [(p+1)*R] penalty weights w_jr (lam_jr = lam_r w_jr), coefficient-major
+  int* use_w;                       // [1] device flag: 0 -> all weights 1 (lamw not read)
   const double* eta;                // [G]
   // state
   double* beta[2];                  // [(p+1)*R], coefficient-major
@@ -61,6 +66,10 @@ struct Dev {
   // K2 partials + last-CTA ticket
   double* k2part;                   // [grid][R][FSQR_NPART]
   unsigned int* ticket;
+  // multi-CTA finalize partials + ticket
+  double* fpart;                    // [FIN_MAXGRID][R][FSQR_FPART]
+  long long* ftsum;                 // [FIN_MAXGRID][R]
+  unsigned int* fticket;
   // per-RHS control
   const double* tau;                // [R]
   double* lam_cur;                  // [R]
@@ -68,6 +77,7 @@ struct Dev {
   int* status;                      // [R]
   long long* commit_iter;           // [R]
   long long* iter;                  // [1]
+  long long* kbase;                 // [1] iteration at which the current solve call started (max_iter is per call)
   int* stop;                        // [1]
   double* lastR;                    // [R][FSQR_TRACE_W]
   double* trace;                    // [trace_cap][R][FSQR_TRACE_W]
@@ -92,6 +102,14 @@ struct Dev {
 };
 
 // ------------------------------------------------------------------ helpers
+
+// column of sample i in the theta digit rows: natural order, or (bperm) the K order of the
+// 2-bit tensor-core kernel, kappa = 128q + 4u + b for sample s = 16u + 4b + q of each 512-block
+__device__ __forceinline__ int bq_index(const Dev& D, int i) {
+  if (!D.bperm) return i;
+  const int s = i & 511;
+  return (i & ~511) | ((s & 3) << 7) | ((s >> 4) << 2) | ((s >> 2) & 3);
+}
 
 __device__ __forceinline__ int block_of_col(const Dev& D, int64_t j) {
   // contiguous near-equal blocks of the p+1 model columns (first `grem` blocks hold q+1)
@@ -131,6 +149,38 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// Deterministic sum of NV values over `count` per-CTA partial records (record b at
+// base + b*stride) by a whole block: thread t adds records t, t+blockDim, ... in order,
+// then a fixed-shape butterfly within warps and a fixed-order sum across warps.  The
+// result depends only on (count, blockDim), never on scheduling.  `sm` needs
+// 32*NV + NV doubles.  Every thread of the block must call it; all receive the sums.
+template <int NV>
+__device__ __forceinline__ void reduce_records(const double* base, int count, int stride, double (&out)[NV],
+                                               double* sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double v[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) v[q] = 0.0;
+  for (int b = threadIdx.x; b < count; b += blockDim.x)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) v[q] += base[(size_t)b * stride + q];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    const double x = warp_sum_d(v[q]);
+    if (lane == 0) sm[wid * NV + q] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double a = 0.0;
+    for (int w = 0; w < nw; ++w) a += sm[w * NV + threadIdx.x];
+    sm[32 * NV + threadIdx.x] = a;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) out[q] = sm[32 * NV + q];
+  __syncthreads();
 }
 
 // ------------------------------------------------------------------ PTX: mbarrier / TMA / tcgen05
@@ -176,6 +226,18 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 }
 __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+
+// one lane of a converged warp (the tcgen05.mma issuer); operands computed before the branch stay
+// warp-uniform, so ptxas keeps them in uniform registers (no per-MMA waterfall)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, P;\n}"
+      : "=r"(p));
+  return p != 0;
 }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -225,6 +287,7 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 template <int RMAX>
 struct K2Ctx {
   long long k;
+  bool use_w;
   const double* beta_in;
   double* beta_out;
   int32_t* sidx;
@@ -262,7 +325,6 @@ __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, i
                                            K2Part<RMAX>& P, double* cval, double* bval) {
   const int64_t j = c + 1;
   const double isd = D.inv_sd[c];
-  const double w = D.lamw ? D.lamw[j] : 1.0;
   const double eta = D.eta[block_of_col(D, j)];
   bool nz = false;
 #pragma unroll
@@ -271,7 +333,7 @@ __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, i
     bval[r] = 0.0;
     if (r >= C.R || !C.active[r]) continue;
     const double b = C.beta_in[j * C.R + r];
-    const double lam = C.lam[r] * w;
+    const double lam = C.use_w ? C.lam[r] * D.lamw[j * C.R + r] : C.lam[r];
     // KKT residual part of w^k and penalty at beta^k
     const double d = b - soft_thr(b + g[r], lam);
     P.v[r][0] += d * d;
@@ -333,9 +395,12 @@ struct LaunchCfg {
 };
 
 void launch_k2_tc(const Dev& D, const void* tmX, const void* tmB, int grid, cudaStream_t st);
+void launch_k2_tc2(const Dev& D, const void* tmX, const void* tmB, int grid, cudaStream_t st);
+cudaError_t k2_tc2_init();
 void launch_k2_simt(const Dev& D, int grid, cudaStream_t st);
 void launch_k1(const Dev& D, int grid, cudaStream_t st);
 void launch_finalize(const Dev& D, cudaStream_t st);
 int k2_tc_smem_bytes(int npad);
 cudaError_t k2_tc_init();
+cudaError_t k1_init();
 int k2_tc_supported(int npad);

@@ -3,186 +3,280 @@
 // by computing their sum"), restricted to the support of beta^{k+1}: only the
 // columns listed by the a2 epilogue are read (n * |S| bytes).
 //
-// Genotype storage: a CTA owns a slab of 32*RPL rows and a slice of support
-// entries; its 8 warps take 32-entry groups of the slice round-robin.  A lane
-// stages one entry of the group (column index and the int64 fixed-point
-// C_j = round(2^E beta_j / s_j), split into 22-bit low / signed high halves),
-// the warp broadcasts them with shuffles and keeps four 128-bit column loads in
-// flight while it accumulates x * C_lo and x * C_hi in int32 registers (exact:
-// |x C| < 2^23 and at most 256 entries per flush).  Warp partials meet in
-// shared memory and leave the CTA as one 64-bit integer atomic per row, so the
-// cross-block sum (the paper's barrier aggregation) is exact and independent of
-// scheduling.  The centring term sum_j colsum_j C_j is accumulated the same
-// way; finalize forms s_i = 2^-E (n S_i - M)/n + beta_0.
-// fp32 storage: one thread per row walks the columns in ascending order (fp64),
-// deterministic by construction (small designs only).
+// Genotype storage (k1_bulk): a persistent CTA takes work items = (row slab of
+// RPW = 256*RPT rows) x (slice of the support list).  A producer warp turns 32
+// support entries at a time into int64 fixed-point coefficients
+// C_j = round(2^E beta_j / s_j) (split into 22-bit low / signed high halves,
+// written to shared memory with each column's slot) and issues one
+// cp.async.bulk copy per entry of the column's slab segment (contiguous bytes)
+// into an mbarrier ring, so the copy engine -- not registers -- keeps the bytes
+// in flight.  Eight consumer warps each own RPT consecutive rows per thread and
+// accumulate x * C_lo and x * C_hi in int32 registers (exact: |x C| < 2^23 and
+// at most 256 entries per flush into int64).  Each thread owns its rows, so a
+// work item leaves the CTA as one 64-bit integer atomic per row and RHS: the
+// cross-block sum (the paper's barrier aggregation, L287) is exact and
+// independent of scheduling.  The centring term sum_j colsum_j C_j is summed by
+// the producer on slab 0; finalize forms s_i = 2^-E (n S_i - M)/n + beta_0.
 #include "fsqr_dev.cuh"
 
 namespace {
 
 constexpr int THREADS = 256;
-constexpr int NWARP = THREADS / 32;
-constexpr int UNR = 4;   // column loads in flight per lane
+constexpr int NCW = 8;              // consumer warps
+constexpr int KTHREADS = 32 * (NCW + 1);
 
-template <int RPL>
-struct Codes {
-  uint32_t w[(RPL + 3) / 4];   // u8: RPL bytes; 2-bit: RPL codes packed (RPL/4 bytes)
-};
-
-template <int RPL, int ST>
-__device__ __forceinline__ void load_codes(const uint8_t* col, int row0, bool inb, Codes<RPL>& c) {
-  if (!inb) {
-#pragma unroll
-    for (int q = 0; q < (RPL + 3) / 4; ++q) c.w[q] = 0;
-    return;
-  }
-  if (ST == 1) {
-    if (RPL == 16) {
-      const uint4 v = __ldcs((const uint4*)(col + row0));
-      c.w[0] = v.x; c.w[1] = v.y; c.w[2] = v.z; c.w[3] = v.w;
-    } else if (RPL == 8) {
-      const uint2 v = __ldcs((const uint2*)(col + row0));
-      c.w[0] = v.x; c.w[1] = v.y;
-    } else {
-      c.w[0] = __ldcs((const uint32_t*)(col + row0));
-    }
-  } else {
-    uint32_t v;
-    if (RPL == 16) v = __ldcs((const uint32_t*)(col + (row0 >> 2)));
-    else if (RPL == 8) v = __ldcs((const uint16_t*)(col + (row0 >> 2)));
-    else v = __ldcs(col + (row0 >> 2));
-    c.w[0] = v;
-  }
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
 }
 
-template <int RPL, int ST>
-__device__ __forceinline__ uint32_t code_at(const Codes<RPL>& c, int i) {
-  if (ST == 1) return (c.w[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-  return (c.w[0] >> (2 * i)) & 3u;
+// rows per thread: keep 4 * RPT * RMAX int32-equivalent accumulator registers <= 64
+template <int RMAX>
+struct K1Shape {
+  static constexpr int RPT = RMAX <= 2 ? 8 : (RMAX <= 4 ? 4 : (RMAX <= 8 ? 2 : 1));
+  static constexpr int RPW = 256 * RPT;
+};
+
+// codes of rows t*RPT .. t*RPT+RPT-1 of one slab segment in shared memory
+template <int RPT, int ST>
+__device__ __forceinline__ void seg_codes(const uint8_t* seg, int t, uint32_t (&x)[RPT]) {
+  if (ST == 1) {
+    if (RPT == 8) {
+      const uint2 v = *(const uint2*)(seg + 8 * t);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        x[q] = (v.x >> (8 * q)) & 0xFFu;
+        x[4 + q] = (v.y >> (8 * q)) & 0xFFu;
+      }
+    } else if (RPT == 4) {
+      const uint32_t v = *(const uint32_t*)(seg + 4 * t);
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) x[q] = (v >> (8 * q)) & 0xFFu;
+    } else if (RPT == 2) {
+      const uint32_t v = *(const uint16_t*)(seg + 2 * t);
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) x[q] = (v >> (8 * q)) & 0xFFu;
+    } else {
+      x[0] = seg[t];
+    }
+  } else {
+    // 2-bit: row i at bits 2(i%4) of byte i/4
+    if (RPT == 8) {
+      const uint32_t v = *(const uint16_t*)(seg + 2 * t);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) x[q] = (v >> (2 * q)) & 3u;
+    } else if (RPT == 4) {
+      const uint32_t v = seg[t];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) x[q] = (v >> (2 * q)) & 3u;
+    } else {
+      const int i0 = t * RPT;
+      const uint32_t v = seg[i0 >> 2] >> (2 * (i0 & 3));
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) x[q] = (v >> (2 * q)) & 3u;
+    }
+  }
 }
 
 template <int RMAX, int ST>
-__global__ void __launch_bounds__(THREADS) k1_int(const Dev D, int cur) {
-  constexpr int RPL = RMAX <= 2 ? 16 : (RMAX <= 4 ? 8 : 4);
-  constexpr int RPW = 32 * RPL;   // rows per slab
-  __shared__ unsigned long long sacc[RPW * RMAX];
-  __shared__ unsigned long long smt[RMAX];
+struct K1Smem {
+  static constexpr int RPT = K1Shape<RMAX>::RPT;
+  static constexpr int SEG = ST == 1 ? 256 * RPT : 64 * RPT;   // bytes of one column's slab segment
+  static constexpr int QC = SEG >= 2048 ? 8 : (SEG >= 1024 ? 16 : 32);   // columns per stage (divides 32)
+  static constexpr int ST0 = (96 * 1024) / (QC * SEG);
+  static constexpr int STAGES = ST0 < 4 ? 4 : (ST0 > 12 ? 12 : ST0);
+  static constexpr int DATA = STAGES * QC * SEG;
+  static constexpr int COEF = STAGES * QC * RMAX * 2 * 4;      // int32 lo/hi per slot and RHS
+  static constexpr int BYTES = 128 + DATA + COEF + 2 * STAGES * 8 + 64;
+};
+
+template <int RMAX, int ST>
+__global__ void __launch_bounds__(KTHREADS) k1_bulk(const Dev D, int cur) {
+  using SH = K1Smem<RMAX, ST>;
+  constexpr int QC = SH::QC;
+  constexpr int STAGES = SH::STAGES;
+  constexpr int RPT = SH::RPT;
+  constexpr int RPW = 256 * RPT;
+  constexpr int SEG = SH::SEG;
+  extern __shared__ uint8_t k1_smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)k1_smem_raw + 127) & ~(uintptr_t)127);
+  uint8_t* sdata = sm;
+  int32_t* scoef = (int32_t*)(sm + SH::DATA);
+  uint64_t* full = (uint64_t*)(sm + SH::DATA + SH::COEF);
+  uint64_t* empty = full + STAGES;
+
   if (*D.stop) return;
   const long long k = *D.iter;
   const int par = (int)((k + (cur ? 0 : 1)) & 1);
   const int cnt = D.sup_cnt[par];
   if (cnt == 0) return;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   const int R = D.R;
-  double scale[RMAX];
-  bool act[RMAX];
-#pragma unroll
-  for (int r = 0; r < RMAX; ++r) {
-    act[r] = r < R && (cur || D.status[r] == ST_ACTIVE);
-    const double cm = r < R ? __longlong_as_double((long long)D.cmax[par * R + r]) : 0.0;
-    scale[r] = ldexp(1.0, fwd_exponent(cm, cnt, D.n));
-  }
-  const int nrc = (D.n + RPW - 1) / RPW;
-  // entries per CTA slice: balance nrc * nslices ~ gridDim, at least one 32-group per warp
-  int64_t es = ((int64_t)cnt * nrc + gridDim.x - 1) / gridDim.x;
-  es = ((es + 32 * NWARP - 1) / (32 * NWARP)) * (32 * NWARP);
-  const int64_t nsl = (cnt + es - 1) / es;
-  const int64_t nwork = nsl * nrc;
+
+  const int nslab = (D.n + RPW - 1) / RPW;
+  // slices per slab so that every CTA gets about one work item; 32-entry granularity
+  const int per = max(1, (int)gridDim.x / nslab);
+  int64_t es = ((int64_t)cnt + per - 1) / per;
+  es = ((es + 31) / 32) * 32;
+  const int64_t nsl = ((int64_t)cnt + es - 1) / es;
+  const int64_t nwork = nsl * nslab;
   const int32_t* sidx = D.sup_idx[par];
   const double* sc = D.sup_c[par];
-  for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
-    const int rc = (int)(w % nrc);
-    const int64_t e0 = (w / nrc) * es, e1 = min((int64_t)cnt, e0 + es);
-    for (int q = threadIdx.x; q < RPW * RMAX; q += THREADS) sacc[q] = 0ull;
-    if (threadIdx.x < RMAX) smt[threadIdx.x] = 0ull;
-    __syncthreads();
-    const int row0 = rc * RPW + lane * RPL;
-    const bool inb = (ST == 1) ? (row0 < D.ld) : ((row0 >> 2) < D.ld);
-    long long acc[RPL][RMAX];
+  const int64_t seg_stride = (ST == 1) ? RPW : RPW / 4;    // bytes between slabs within a column
+
+  if (tid == 0) {
+    for (int q = 0; q < STAGES; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (wid == NCW) {
+    // ===================== producer warp
+    double scale[RMAX];
+    bool act[RMAX];
 #pragma unroll
-    for (int i = 0; i < RPL; ++i)
+    for (int r = 0; r < RMAX; ++r) {
+      act[r] = r < R && (cur || D.status[r] == ST_ACTIVE);
+      const double cm = r < R ? __longlong_as_double((long long)D.cmax[par * R + r]) : 0.0;
+      scale[r] = ldexp(1.0, fwd_exponent(cm, cnt, D.n));
+    }
+    const uint64_t pol = policy_evict_first();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+      const int slab = (int)(w % nslab);
+      const int64_t e0 = (w / nslab) * es, e1 = min((int64_t)cnt, e0 + es);
+      const int64_t boff = (int64_t)slab * seg_stride;
+      const uint32_t bytes = (uint32_t)min((int64_t)SEG, D.ld - boff);
+      long long mt[RMAX];
 #pragma unroll
-      for (int r = 0; r < RMAX; ++r) acc[i][r] = 0;
-    long long mt[RMAX];
-#pragma unroll
-    for (int r = 0; r < RMAX; ++r) mt[r] = 0;
-    for (int64_t g0 = e0 + 32 * wid; g0 < e1; g0 += 32 * NWARP) {
-      // stage one entry per lane
-      const int64_t e = g0 + lane;
-      const int ng = (int)min((int64_t)32, e1 - g0);
-      int32_t myc = 0;
-      int32_t clo[RMAX], chi[RMAX];
-      if (e < e1) {
-        myc = sidx[e];
-        const long long cs = (rc == 0) ? (long long)D.colsum[myc] : 0;
-#pragma unroll
-        for (int r = 0; r < RMAX; ++r) {
-          const long long C = act[r] ? __double2ll_rn(sc[e * R + r] * scale[r]) : 0;
-          clo[r] = (int32_t)(C & 0x3FFFFF);
-          chi[r] = (int32_t)(C >> 22);
-          mt[r] += cs * C;
-        }
-      } else {
+      for (int r = 0; r < RMAX; ++r) mt[r] = 0;
+      for (int64_t g0 = e0; g0 < e1; g0 += 32) {
+        const int64_t e = g0 + lane;
+        int32_t col = 0;
+        int32_t clo[RMAX], chi[RMAX];
 #pragma unroll
         for (int r = 0; r < RMAX; ++r) clo[r] = chi[r] = 0;
-      }
-      int32_t alo[RPL][RMAX], ahi[RPL][RMAX];
-#pragma unroll
-      for (int i = 0; i < RPL; ++i)
-#pragma unroll
-        for (int r = 0; r < RMAX; ++r) alo[i][r] = ahi[i][r] = 0;
-      for (int u0 = 0; u0 < ng; u0 += UNR) {
-        Codes<RPL> cd[UNR];
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-          const int cu = __shfl_sync(0xffffffffu, myc, (u0 + u) & 31);
-          load_codes<RPL, ST>(D.X8 + (int64_t)cu * D.ld, row0, inb && (u0 + u < ng), cd[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
+        if (e < e1) {
+          col = sidx[e];
+          const long long cs = (slab == 0) ? (long long)D.colsum[col] : 0;
 #pragma unroll
           for (int r = 0; r < RMAX; ++r) {
-            const int32_t lo = __shfl_sync(0xffffffffu, clo[r], (u0 + u) & 31);
-            const int32_t hi = __shfl_sync(0xffffffffu, chi[r], (u0 + u) & 31);
+            const long long C = act[r] ? __double2ll_rn(sc[e * R + r] * scale[r]) : 0;
+            clo[r] = (int32_t)(C & 0x3FFFFF);
+            chi[r] = (int32_t)(C >> 22);
+            mt[r] += cs * C;
+          }
+        }
+        const int ng = (int)min((int64_t)32, e1 - g0);
+        for (int q0 = 0; q0 < ng; q0 += QC) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          // slot q of this stage <- entry q0 + q of the group (lanes q0 .. q0+QC-1)
+          const int q = lane - q0;
+          if (q >= 0 && q < QC) {
+            int32_t* cf = scoef + (stage * QC + q) * RMAX * 2;
+            const bool live = lane < ng;
 #pragma unroll
-            for (int i = 0; i < RPL; ++i) {
-              const int32_t x = (int32_t)code_at<RPL, ST>(cd[u], i);
-              alo[i][r] += x * lo;
-              ahi[i][r] += x * hi;
+            for (int r = 0; r < RMAX; ++r) {
+              cf[2 * r] = live ? clo[r] : 0;
+              cf[2 * r + 1] = live ? chi[r] : 0;
             }
+          }
+          __syncwarp();
+          const int nq = min(QC, ng - q0);
+          if (lane == 0) mbar_expect_tx(&full[stage], bytes * (uint32_t)nq);
+          // every lane holding a column of this stage issues its own copy (lane q0+u)
+          if (q >= 0 && q < nq)
+            bulk_g2s(sdata + (stage * QC + q) * SEG, D.X8 + (int64_t)col * D.ld + boff, bytes, &full[stage], pol);
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
           }
         }
       }
+      if (slab == 0) {
 #pragma unroll
-      for (int i = 0; i < RPL; ++i)
+        for (int r = 0; r < RMAX; ++r) {
+          long long v = mt[r];
 #pragma unroll
-        for (int r = 0; r < RMAX; ++r)
-          acc[i][r] += (long long)(uint32_t)alo[i][r] + ((long long)ahi[i][r] << 22);
-    }
-    // warp partials -> shared (exact integer atomics) -> one global atomic per row
-#pragma unroll
-    for (int i = 0; i < RPL; ++i)
-#pragma unroll
-      for (int r = 0; r < RMAX; ++r)
-        if (act[r] && acc[i][r] != 0) atomicAdd(&sacc[(lane * RPL + i) * RMAX + r], (unsigned long long)acc[i][r]);
-    if (rc == 0) {
-#pragma unroll
-      for (int r = 0; r < RMAX; ++r) {
-        long long v = mt[r];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0 && v != 0) atomicAdd(&smt[r], (unsigned long long)v);
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          if (lane == 0 && v != 0) atomicAdd((unsigned long long*)&D.mterm[r], (unsigned long long)v);
+        }
       }
     }
-    __syncthreads();
-    for (int q = threadIdx.x; q < RPW * RMAX; q += THREADS) {
-      const int row = rc * RPW + q / RMAX, r = q % RMAX;
-      const unsigned long long v = sacc[q];
-      if (row < D.n && r < R && v != 0ull) atomicAdd((unsigned long long*)&D.sacc[(int64_t)r * D.n + row], v);
+  } else {
+    // ===================== consumer warps: thread t owns rows slab*RPW + t*RPT .. +RPT-1
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+      const int slab = (int)(w % nslab);
+      const int64_t e0 = (w / nslab) * es, e1 = min((int64_t)cnt, e0 + es);
+      long long acc[RPT][RMAX];
+#pragma unroll
+      for (int i = 0; i < RPT; ++i)
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r) acc[i][r] = 0;
+      int32_t alo[RPT][RMAX], ahi[RPT][RMAX];
+#pragma unroll
+      for (int i = 0; i < RPT; ++i)
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r) alo[i][r] = ahi[i][r] = 0;
+      int since = 0;
+      for (int64_t g0 = e0; g0 < e1; g0 += 32) {
+        const int ng = (int)min((int64_t)32, e1 - g0);
+        for (int q0 = 0; q0 < ng; q0 += QC) {
+          mbar_wait(&full[stage], phase);
+          const int nq = min(QC, ng - q0);
+          const uint8_t* sd = sdata + stage * QC * SEG;
+          const int32_t* cf = scoef + stage * QC * RMAX * 2;
+          for (int q = 0; q < nq; ++q) {
+            uint32_t x[RPT];
+            seg_codes<RPT, ST>(sd + q * SEG, tid, x);
+#pragma unroll
+            for (int r = 0; r < RMAX; ++r) {
+              const int32_t lo = cf[(q * RMAX + r) * 2], hi = cf[(q * RMAX + r) * 2 + 1];
+#pragma unroll
+              for (int i = 0; i < RPT; ++i) {
+                alo[i][r] += (int32_t)x[i] * lo;
+                ahi[i][r] += (int32_t)x[i] * hi;
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+          since += nq;
+          if (since >= 256 - QC) {
+#pragma unroll
+            for (int i = 0; i < RPT; ++i)
+#pragma unroll
+              for (int r = 0; r < RMAX; ++r) {
+                acc[i][r] += (long long)(uint32_t)alo[i][r] + ((long long)ahi[i][r] << 22);
+                alo[i][r] = ahi[i][r] = 0;
+              }
+            since = 0;
+          }
+        }
+      }
+      const int rowb = slab * RPW + tid * RPT;
+#pragma unroll
+      for (int i = 0; i < RPT; ++i)
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r) {
+          const long long v = acc[i][r] + (long long)(uint32_t)alo[i][r] + ((long long)ahi[i][r] << 22);
+          if (r < R && rowb + i < D.n && v != 0)
+            atomicAdd((unsigned long long*)&D.sacc[(int64_t)r * D.n + rowb + i], (unsigned long long)v);
+        }
     }
-    if (rc == 0 && threadIdx.x < R && smt[threadIdx.x] != 0ull)
-      atomicAdd((unsigned long long*)&D.mterm[threadIdx.x], smt[threadIdx.x]);
-    __syncthreads();
   }
 }
 
@@ -216,18 +310,34 @@ __global__ void __launch_bounds__(THREADS) k1_f32(const Dev D, int cur) {
   }
 }
 
+template <int RMAX, int ST>
+int bulk_grid(int grid) {
+  // persistent: as many CTAs as fit (shared memory bound), grid = 148 x that by default
+  const int per_sm = (200 * 1024) / K1Smem<RMAX, ST>::BYTES;
+  return grid * (per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm));
+}
+
 template <int RMAX>
 void launch_r(const Dev& D, int grid, cudaStream_t st, int cur) {
   if (D.storage == 0)
     k1_f32<RMAX><<<(D.n + THREADS - 1) / THREADS, THREADS, 0, st>>>(D, cur);
   else if (D.storage == 1)
-    k1_int<RMAX, 1><<<grid, THREADS, 0, st>>>(D, cur);
+    k1_bulk<RMAX, 1><<<bulk_grid<RMAX, 1>(grid), KTHREADS, K1Smem<RMAX, 1>::BYTES, st>>>(D, cur);
   else
-    k1_int<RMAX, 2><<<grid, THREADS, 0, st>>>(D, cur);
+    k1_bulk<RMAX, 2><<<bulk_grid<RMAX, 2>(grid), KTHREADS, K1Smem<RMAX, 2>::BYTES, st>>>(D, cur);
+}
+
+template <int RMAX>
+cudaError_t init_r() {
+  cudaError_t e = cudaFuncSetAttribute(k1_bulk<RMAX, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       K1Smem<RMAX, 1>::BYTES);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k1_bulk<RMAX, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, K1Smem<RMAX, 2>::BYTES);
 }
 
 }  // namespace
 
+// grid = number of SMs; the bulk kernel scales it by its resident CTAs per SM
 void launch_k1_mode(const Dev& D, int grid, cudaStream_t st, int cur) {
   if (D.R <= 1) launch_r<1>(D, grid, st, cur);
   else if (D.R <= 2) launch_r<2>(D, grid, st, cur);
@@ -237,3 +347,12 @@ void launch_k1_mode(const Dev& D, int grid, cudaStream_t st, int cur) {
 }
 
 void launch_k1(const Dev& D, int grid, cudaStream_t st) { launch_k1_mode(D, grid, st, 0); }
+
+cudaError_t k1_init() {
+  cudaError_t e;
+  if ((e = init_r<1>()) != cudaSuccess) return e;
+  if ((e = init_r<2>()) != cudaSuccess) return e;
+  if ((e = init_r<4>()) != cudaSuccess) return e;
+  if ((e = init_r<8>()) != cudaSuccess) return e;
+  return init_r<16>();
+}

@@ -7,6 +7,7 @@
 template <int RMAX>
 __device__ void k2_load_ctx(const Dev& D, K2Ctx<RMAX>& C) {
   C.k = *D.iter;
+  C.use_w = *D.use_w != 0;
   const int par = (int)(C.k & 1);
   C.beta_in = D.beta[par];
   C.beta_out = D.beta[par ^ 1];
@@ -69,15 +70,22 @@ __device__ void k2_finish(const Dev& D, const K2Ctx<RMAX>& C, K2Part<RMAX>& P, d
   if (!s_last) return;
   __threadfence();
 
-  // ---------------- last CTA: R(w^k) for every active RHS (fixed-order sum over CTAs)
+  // ---------------- last CTA: R(w^k) for every active RHS (deterministic block sum over CTAs)
   __shared__ int s_rec[FSQR_MAXR];
+  __shared__ double s_tot[FSQR_MAXR][FSQR_NPART];
+  for (int r = 0; r < C.R; ++r) {
+    double t5[FSQR_NPART];
+    reduce_records<FSQR_NPART>(D.k2part + (size_t)r * FSQR_NPART, (int)gridDim.x, D.R * FSQR_NPART, t5, red);
+    if (tid == 0)
+      for (int q = 0; q < FSQR_NPART; ++q) s_tot[r][q] = t5[q];
+  }
+  __syncthreads();
   if (tid < C.R) {
     const int r = tid;
     s_rec[r] = -1;
     if (C.active[r]) {
-      double a[FSQR_NPART] = {0, 0, 0, 0, 0};
-      for (int b = 0; b < (int)gridDim.x; ++b)
-        for (int q = 0; q < FSQR_NPART; ++q) a[q] += D.k2part[((size_t)b * D.R + r) * FSQR_NPART + q];
+      double a[FSQR_NPART];
+      for (int q = 0; q < FSQR_NPART; ++q) a[q] = s_tot[r][q];
       const double g0 = D.sumth[r], b0 = C.beta_in[r];
       const double rb = a[0] + g0 * g0, bb = a[1] + b0 * b0, gg = a[2] + g0 * g0;
       const double Rb = sqrt(rb) / (1.0 + sqrt(bb) + sqrt(gg));
@@ -127,7 +135,7 @@ __device__ void k2_finish(const Dev& D, const K2Ctx<RMAX>& C, K2Part<RMAX>& P, d
           if (Rm <= D.tol) {
             D.status[r] = ST_CONVERGED;
             D.commit_iter[r] = C.k;
-          } else if (C.k >= D.max_iter) {
+          } else if (C.k - *D.kbase >= D.max_iter) {
             D.status[r] = ST_MAXITER;
             D.commit_iter[r] = C.k;
           }

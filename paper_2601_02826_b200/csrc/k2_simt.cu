@@ -14,6 +14,7 @@
 namespace {
 
 constexpr int THREADS = 256;
+#define K2_RED_DOUBLES(RM) ((THREADS / 32) * (RM) * (FSQR_NPART + 1) > 33 * FSQR_NPART ? (THREADS / 32) * (RM) * (FSQR_NPART + 1) : 33 * FSQR_NPART)
 
 __device__ __forceinline__ uint32_t unpack2(uint32_t b) {
   // byte of four 2-bit codes -> four bytes {0,1,2}
@@ -24,7 +25,7 @@ template <int RMAX, int ST>
 __global__ void __launch_bounds__(THREADS) k2_simt_int(const Dev D) {
   constexpr int CPW = RMAX <= 2 ? 4 : (RMAX <= 4 ? 2 : 1);   // columns per warp
   constexpr int ND = 4 * RMAX;                                 // digit rows
-  __shared__ double red[(THREADS / 32) * RMAX * (FSQR_NPART + 1)];
+  __shared__ double red[K2_RED_DOUBLES(RMAX)];
   if (*D.stop) return;
   K2Ctx<RMAX> C;
   k2_load_ctx(D, C);
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(THREADS) k2_simt_int(const Dev D) {
 
 template <int RMAX>
 __global__ void __launch_bounds__(THREADS) k2_simt_f32(const Dev D) {
-  __shared__ double red[(THREADS / 32) * RMAX * (FSQR_NPART + 1)];
+  __shared__ double red[K2_RED_DOUBLES(RMAX)];
   if (*D.stop) return;
   K2Ctx<RMAX> C;
   k2_load_ctx(D, C);

@@ -28,21 +28,22 @@ constexpr int TILE_K = 128;   // bytes of K per stage (one 128B swizzle row)
 constexpr int A_BYTES = TILE_M * TILE_K;
 constexpr int THREADS = 256;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4..7 epilogue
 
-template <int NPAD>
+template <int NPAD, int RM>
 struct Cfg {
   static constexpr int B_BYTES = NPAD * TILE_K;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = (200 * 1024) / STAGE;
-  static constexpr int RMAX = NPAD / 4;
+  static constexpr int RMAX = RM;   // RHS slots compiled in (<= NPAD / 4)
   static constexpr int TMEM_COLS = (2 * NPAD <= 32) ? 32 : (2 * NPAD <= 64 ? 64 : (2 * NPAD <= 128 ? 128 : 256));
-  static constexpr int RED_DOUBLES = (THREADS / 32) * RMAX * (FSQR_NPART + 1);
+  static constexpr int RED0 = (THREADS / 32) * RMAX * (FSQR_NPART + 1);
+  static constexpr int RED_DOUBLES = RED0 > 33 * FSQR_NPART ? RED0 : 33 * FSQR_NPART;
   static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE + 1024 /*barriers*/ + RED_DOUBLES * 8;
 };
 
-template <int NPAD>
+template <int NPAD, int RM>
 __global__ void __launch_bounds__(THREADS, 1)
     k2_tc_kernel(const Dev D, const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmB) {
-  using CF = Cfg<NPAD>;
+  using CF = Cfg<NPAD, RM>;
   constexpr int RMAX = CF::RMAX;
   if (*D.stop) return;
   extern __shared__ uint8_t smem_raw[];
@@ -84,23 +85,40 @@ __global__ void __launch_bounds__(THREADS, 1)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
+  // digit rows 4R..NPAD-1 of every B stage are never loaded (the TMA box has 4R rows): zero them
+  // once, then make the generic-proxy stores visible to the tensor core's async proxy
+  {
+    constexpr int BROW = 128;   // bytes of one digit row per stage
+    const int live = 4 * D.R;
+    for (int s = 0; s < CF::STAGES; ++s)
+      for (int a = 0; a < 1; ++a) {
+        uint8_t* base = sB + s * CF::B_BYTES + a * NPAD * 128;
+        for (int q = live * 128 + tid * 16; q < NPAD * 128; q += THREADS * 16) *(uint4*)(base + q) = make_uint4(0, 0, 0, 0);
+      }
+    (void)BROW;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (wid == 0) {
-    // ===== TMA producer =====
-    if (lane == 0) {
+    // ===== TMA producer: the whole warp walks the ring, one elected lane issues =====
+    {
       const uint64_t pol_x = policy_evict_first(), pol_b = policy_evict_last();
+      const uint32_t bytes = (uint32_t)(A_BYTES + 4 * D.R * 128);
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], (uint32_t)CF::STAGE);
-          tma_load_2d(sA + stage * A_BYTES, &tmX, &full[stage], kb * TILE_K, (int)(t * TILE_M), pol_x);
-          tma_load_2d(sB + stage * CF::B_BYTES, &tmB, &full[stage], kb * TILE_K, 0, pol_b);
+          if (elect_one()) {
+            mbar_expect_tx(&full[stage], bytes);
+            tma_load_2d(sA + stage * A_BYTES, &tmX, &full[stage], kb * TILE_K, (int)(t * TILE_M), pol_x);
+            tma_load_2d(sB + stage * CF::B_BYTES, &tmB, &full[stage], kb * TILE_K, 0, pol_b);
+          }
+          __syncwarp();
           if (++stage == CF::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -109,9 +127,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (wid == 1) {
-    // ===== MMA issuer (single thread) =====
-    if (lane == 0) {
+    // ===== MMA issuer: the whole warp walks the pipeline, one elected lane issues =====
+    {
       constexpr uint32_t idesc = idesc_i8(NPAD);
+      const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
+      const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB);
       int stage = 0;
       uint32_t phase = 0;
       int lt = 0;
@@ -120,22 +140,26 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t aph = (lt >> 1) & 1;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * NPAD);
+        const uint32_t d_tmem = tbase + (uint32_t)(acc * NPAD);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint64_t adesc = umma_desc_sw128(smem_u32(sA + stage * A_BYTES));
-          const uint64_t bdesc = umma_desc_sw128(smem_u32(sB + stage * CF::B_BYTES));
+          const uint64_t adesc = umma_desc_sw128(sA0 + (uint32_t)(stage * A_BYTES));
+          const uint64_t bdesc = umma_desc_sw128(sB0 + (uint32_t)(stage * CF::B_BYTES));
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < TILE_K / 32; ++k)   // K = 32 bytes per kind::i8 MMA
-            umma_i8(d_tmem, adesc + (uint64_t)(2 * k), bdesc + (uint64_t)(2 * k), idesc, (kb | k) != 0);
-          umma_commit(&empty[stage]);
+            for (int k = 0; k < TILE_K / 32; ++k)   // K = 32 bytes per kind::i8 MMA
+              umma_i8(d_tmem, adesc + (uint64_t)(2 * k), bdesc + (uint64_t)(2 * k), idesc, (kb | k) != 0);
+            umma_commit(&empty[stage]);
+          }
+          __syncwarp();
           if (++stage == CF::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);
+        if (elect_one()) umma_commit(&tfull[acc]);
+        __syncwarp();
       }
     }
   } else if (wid >= 4) {
@@ -188,43 +212,43 @@ __global__ void __launch_bounds__(THREADS, 1)
   k2_finish<RMAX>(D, C, P, red);
 }
 
-template <int NPAD>
+template <int NPAD, int RM>
 void launch_np(const Dev& D, const void* tmX, const void* tmB, int grid, cudaStream_t st) {
-  using CF = Cfg<NPAD>;
-  k2_tc_kernel<NPAD><<<grid, THREADS, CF::SMEM, st>>>(D, *(const CUtensorMap*)tmX, *(const CUtensorMap*)tmB);
+  k2_tc_kernel<NPAD, RM><<<grid, THREADS, Cfg<NPAD, RM>::SMEM, st>>>(D, *(const CUtensorMap*)tmX,
+                                                                *(const CUtensorMap*)tmB);
 }
 
-template <int NPAD>
+template <int NPAD, int RM>
 cudaError_t init_np() {
-  return cudaFuncSetAttribute(k2_tc_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<NPAD>::SMEM);
+  return cudaFuncSetAttribute(k2_tc_kernel<NPAD, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<NPAD, RM>::SMEM);
 }
 
 }  // namespace
 
 cudaError_t k2_tc_init() {
   cudaError_t e;
-  if ((e = init_np<16>()) != cudaSuccess) return e;
-  if ((e = init_np<32>()) != cudaSuccess) return e;
-  if ((e = init_np<48>()) != cudaSuccess) return e;
-  return init_np<64>();
+  if ((e = init_np<16, 1>()) != cudaSuccess) return e;
+  if ((e = init_np<16, 4>()) != cudaSuccess) return e;
+  if ((e = init_np<32, 8>()) != cudaSuccess) return e;
+  if ((e = init_np<48, 12>()) != cudaSuccess) return e;
+  return init_np<64, 16>();
 }
 
 int k2_tc_supported(int npad) { return npad == 16 || npad == 32 || npad == 48 || npad == 64; }
 
 int k2_tc_smem_bytes(int npad) {
   switch (npad) {
-    case 16: return Cfg<16>::SMEM;
-    case 32: return Cfg<32>::SMEM;
-    case 48: return Cfg<48>::SMEM;
-    default: return Cfg<64>::SMEM;
+    case 16: return Cfg<16, 4>::SMEM;
+    case 32: return Cfg<32, 8>::SMEM;
+    case 48: return Cfg<48, 12>::SMEM;
+    default: return Cfg<64, 16>::SMEM;
   }
 }
 
 void launch_k2_tc(const Dev& D, const void* tmX, const void* tmB, int grid, cudaStream_t st) {
-  switch (D.npad) {
-    case 16: launch_np<16>(D, tmX, tmB, grid, st); break;
-    case 32: launch_np<32>(D, tmX, tmB, grid, st); break;
-    case 48: launch_np<48>(D, tmX, tmB, grid, st); break;
-    default: launch_np<64>(D, tmX, tmB, grid, st); break;
-  }
+  if (D.R == 1) launch_np<16, 1>(D, tmX, tmB, grid, st);
+  else if (D.npad == 16) launch_np<16, 4>(D, tmX, tmB, grid, st);
+  else if (D.npad == 32) launch_np<32, 8>(D, tmX, tmB, grid, st);
+  else if (D.npad == 48) launch_np<48, 12>(D, tmX, tmB, grid, st);
+  else launch_np<64, 16>(D, tmX, tmB, grid, st);
 }

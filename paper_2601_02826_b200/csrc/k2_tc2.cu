@@ -1,0 +1,333 @@
+// k2_tc2.cu — a1+a2 for 2-bit packed genotypes on the 5th-generation tensor cores.
+//
+// The same pass as k2_tc.cu (g^k = X~^T theta^k; beta prox E14,
+// L274-277; support list; R_beta / penalty partials), for the PACKED2 storage
+// of config C4 (4 samples per byte).  Unpacking 2-bit codes to bytes in shared
+// memory would cost 4x the shared-memory bandwidth of the packed stream, so the
+// unpacked A operand goes to TENSOR MEMORY instead:
+//
+//   TMA (warp 0): 128 columns x 128 packed bytes (= 512 samples) per stage,
+//       SWIZZLE_128B, plus the matching 512-sample slice of the theta digit
+//       planes (four 128-byte swizzle atoms of NPAD rows).
+//   convert (warps 4-7, one TMEM lane quarter each): thread = tile column c
+//       reads its 128 packed bytes (8 conflict-free 16-byte loads thanks to the
+//       swizzle), and for q = 0..3 forms (w >> 2q) & 0x03030303 from each packed
+//       word w -- the codes of samples 16u + 4b + q, one per byte -- and stores
+//       them with tcgen05.st into a 128-column TMEM A buffer (3 buffers).  The
+//       K order inside a 512-sample block is therefore kappa = 128q + 4u + b for
+//       sample s = 16u + 4b + q; the digit planes of theta are written in that
+//       same order by finalize (D.bperm), so the dot products are unchanged.
+//   MMA (warp 1, one thread): 16 x tcgen05.mma.kind::i8 (K = 32) per stage with
+//       A read from TMEM and B from shared memory into a double-buffered int32
+//       accumulator (exact).
+//   epilogue (warps 8-11): identical to k2_tc.cu.
+// X is read from HBM exactly once per iteration; the CUDA cores spend about two
+// instructions per four samples on unpacking.
+#include <cuda.h>
+
+#include "k2_common.cuh"
+
+namespace {
+
+constexpr int TILE_M = 128;               // columns per tile (UMMA M)
+constexpr int PK = 128;                   // packed bytes per column per stage
+constexpr int KS = 4 * PK;                // samples (K) per stage
+constexpr int A_BYTES = TILE_M * PK;      // 16 KB packed A per stage
+constexpr int THREADS = 384;              // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-7 convert, w8-11 epilogue
+constexpr int NAB = 3;                    // TMEM A buffers
+constexpr int A_COLS = KS / 4;            // TMEM columns per A buffer (4 int8 per 32-bit cell)
+constexpr int A_COL0 = 128;               // A buffers start after the accumulators (2*NPAD <= 128)
+
+template <int NPAD, int RM>
+struct Cfg2 {
+  static constexpr int B_ATOM = NPAD * 128;
+  static constexpr int B_BYTES = 4 * B_ATOM;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (192 * 1024) / STAGE;
+  static constexpr int RMAX = RM;   // RHS slots compiled in (<= NPAD / 4)
+  static constexpr int RED0 = (THREADS / 32) * RMAX * (FSQR_NPART + 1);
+  static constexpr int RED_DOUBLES = RED0 > 33 * FSQR_NPART ? RED0 : 33 * FSQR_NPART;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 1024 + RED_DOUBLES * 8;
+};
+
+__device__ __forceinline__ void umma_i8_tmem_a(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]),
+      "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]),
+      "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+template <int NPAD, int RM>
+__global__ void __launch_bounds__(THREADS, 1)
+    k2_tc2_kernel(const Dev D, const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmB) {
+  using CF = Cfg2<NPAD, RM>;
+  constexpr int RMAX = CF::RMAX;
+  if (*D.stop) return;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + CF::STAGES * A_BYTES;
+  uint64_t* full = (uint64_t*)(smem + CF::STAGES * CF::STAGE);
+  uint64_t* empty = full + CF::STAGES;
+  uint64_t* afull = empty + CF::STAGES;
+  uint64_t* aempty = afull + NAB;
+  uint64_t* tfull = aempty + NAB;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  double* red = (double*)(smem + CF::STAGES * CF::STAGE + 1024);
+
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int64_t ntiles = (D.p + TILE_M - 1) / TILE_M;
+  const int kblocks = (int)((D.ld + PK - 1) / PK);
+
+  K2Ctx<RMAX> C;
+  k2_load_ctx(D, C);
+  K2Part<RMAX> P;
+  P.zero();
+
+  if (wid == 0 && lane == 0) {
+    prefetch_tmap(&tmX);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < CF::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < NAB; ++a) {
+      mbar_init(&afull[a], 4);
+      mbar_init(&aempty[a], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+  }
+  if (wid == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  // digit rows 4R..NPAD-1 of every B stage are never loaded (the TMA box has 4R rows): zero them
+  // once, then make the generic-proxy stores visible to the tensor core's async proxy
+  {
+    constexpr int BROW = 512;   // bytes of one digit row per stage
+    const int live = 4 * D.R;
+    for (int s = 0; s < CF::STAGES; ++s)
+      for (int a = 0; a < 4; ++a) {
+        uint8_t* base = sB + s * CF::B_BYTES + a * NPAD * 128;
+        for (int q = live * 128 + tid * 16; q < NPAD * 128; q += THREADS * 16) *(uint4*)(base + q) = make_uint4(0, 0, 0, 0);
+      }
+    (void)BROW;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (wid == 0) {
+    // ===== TMA producer: the whole warp walks the ring, one elected lane issues =====
+    {
+      const uint64_t pol_x = policy_evict_first(), pol_b = policy_evict_last();
+      const uint32_t bytes = (uint32_t)(A_BYTES + 4 * 4 * D.R * 128);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (elect_one()) {
+            mbar_expect_tx(&full[stage], bytes);
+            tma_load_2d(sA + stage * A_BYTES, &tmX, &full[stage], kb * PK, (int)(t * TILE_M), pol_x);
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+              tma_load_2d(sB + stage * CF::B_BYTES + a * CF::B_ATOM, &tmB, &full[stage], kb * KS + a * 128, 0, pol_b);
+          }
+          __syncwarp();
+          if (++stage == CF::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (wid == 1) {
+    // ===== MMA issuer: the whole warp walks the pipeline, one elected lane issues =====
+    {
+      constexpr uint32_t idesc = idesc_i8(NPAD);
+      const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
+      const uint32_t sB0 = smem_u32(sB);
+      int stage = 0, ab = 0;
+      uint32_t phase = 0, aphase = 0;
+      int lt = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+        const int acc = lt & 1;
+        const uint32_t tph = (lt >> 1) & 1;
+        mbar_wait(&tempty[acc], tph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tbase + (uint32_t)(acc * NPAD);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          mbar_wait(&afull[ab], aphase);
+          tc_fence_after();
+          const uint32_t a_tmem = tbase + (uint32_t)(A_COL0 + ab * A_COLS);
+          const uint64_t bdesc0 = umma_desc_sw128(sB0 + (uint32_t)(stage * CF::B_BYTES));
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < KS / 32; ++kk)   // K = 32 samples per kind::i8 MMA
+              umma_i8_tmem_a(d_tmem, a_tmem + (uint32_t)(8 * kk),
+                             bdesc0 + (uint64_t)((kk >> 2) * (CF::B_ATOM >> 4) + 2 * (kk & 3)), idesc, (kb | kk) != 0);
+            umma_commit(&empty[stage]);
+            umma_commit(&aempty[ab]);
+          }
+          __syncwarp();
+          if (++stage == CF::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+          if (++ab == NAB) {
+            ab = 0;
+            aphase ^= 1;
+          }
+        }
+        if (elect_one()) umma_commit(&tfull[acc]);
+        __syncwarp();
+      }
+    }
+  } else if (wid >= 4 && wid < 8) {
+    // ===== converters: thread = tile column 32*(wid-4) + lane = TMEM lane =====
+    const int q4 = wid - 4;
+    const int c = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    int stage = 0, ab = 0;
+    uint32_t phase = 0, aphase = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        mbar_wait(&aempty[ab], aphase ^ 1);
+        tc_fence_after();
+        uint32_t w[32];
+        const uint8_t* row = sA + stage * A_BYTES + c * PK;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {   // logical 16-byte chunk j sits at chunk j ^ (c & 7) (SWIZZLE_128B)
+          const uint4 v = *(const uint4*)(row + ((j ^ (c & 7)) << 4));
+          w[4 * j] = v.x;
+          w[4 * j + 1] = v.y;
+          w[4 * j + 2] = v.z;
+          w[4 * j + 3] = v.w;
+        }
+        const uint32_t abase = tmem_base + lane_off + (uint32_t)(A_COL0 + ab * A_COLS);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t o[32];
+#pragma unroll
+          for (int u = 0; u < 32; ++u) o[u] = (w[u] >> (2 * q)) & 0x03030303u;
+          tmem_st32(abase + (uint32_t)(32 * q), o);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&afull[ab]);
+        if (++stage == CF::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+        if (++ab == NAB) {
+          ab = 0;
+          aphase ^= 1;
+        }
+      }
+    }
+  } else if (wid >= 8) {
+    // ===== epilogue: TMEM lanes 32*(wid-8) .. +31 = columns of the tile =====
+    const int q = wid - 8;
+    int lt = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+      const int acc = lt & 1;
+      const uint32_t aph = (lt >> 1) & 1;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      int32_t dv[NPAD];
+#pragma unroll
+      for (int h = 0; h < NPAD / 16; ++h) {
+        uint32_t v[16];
+        tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NPAD + h * 16), v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 16; ++u) dv[h * 16 + u] = (int32_t)v[u];
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+
+      const int64_t c = t * TILE_M + q * 32 + lane;
+      bool nz = false;
+      double cval[RMAX], bval[RMAX];
+      if (c < D.p) {
+        double g[RMAX];
+        const int32_t cs = D.colsum[c];
+        const double isd = D.inv_sd[c];
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r)
+          g[r] = r < C.R ? g_from_digits(D.n, cs, C.Tsum[r], C.gscale[r], isd, dv + 4 * r) : 0.0;
+        nz = epi_column<RMAX>(D, C, c, g, P, cval, bval);
+      } else {
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r) cval[r] = bval[r] = 0.0;
+      }
+      if (D.update) support_append<RMAX>(C, nz, c, cval, bval);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (wid == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
+  }
+  k2_finish<RMAX>(D, C, P, red);
+}
+
+template <int NPAD, int RM>
+void launch_np(const Dev& D, const void* tmX, const void* tmB, int grid, cudaStream_t st) {
+  k2_tc2_kernel<NPAD, RM><<<grid, THREADS, Cfg2<NPAD, RM>::SMEM, st>>>(D, *(const CUtensorMap*)tmX,
+                                                                *(const CUtensorMap*)tmB);
+}
+
+template <int NPAD, int RM>
+cudaError_t init_np() {
+  return cudaFuncSetAttribute(k2_tc2_kernel<NPAD, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<NPAD, RM>::SMEM);
+}
+
+}  // namespace
+
+cudaError_t k2_tc2_init() {
+  cudaError_t e;
+  if ((e = init_np<16, 1>()) != cudaSuccess) return e;
+  if ((e = init_np<16, 4>()) != cudaSuccess) return e;
+  if ((e = init_np<32, 8>()) != cudaSuccess) return e;
+  if ((e = init_np<48, 12>()) != cudaSuccess) return e;
+  return init_np<64, 16>();
+}
+
+void launch_k2_tc2(const Dev& D, const void* tmX, const void* tmB, int grid, cudaStream_t st) {
+  if (D.R == 1) launch_np<16, 1>(D, tmX, tmB, grid, st);
+  else if (D.npad == 16) launch_np<16, 4>(D, tmX, tmB, grid, st);
+  else if (D.npad == 32) launch_np<32, 8>(D, tmX, tmB, grid, st);
+  else if (D.npad == 48) launch_np<48, 12>(D, tmX, tmB, grid, st);
+  else launch_np<64, 16>(D, tmX, tmB, grid, st);
+}

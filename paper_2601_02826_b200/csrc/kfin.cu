@@ -97,10 +97,11 @@ __device__ void quantize_theta(const Dev& D, int r, double mx, long long* smll) 
     T = (T - d2) >> 8;
     const int d1 = (int)(int8_t)(T & 0xFF);
     T = (T - d1) >> 8;
-    b0[i] = (int8_t)T;
-    b0[D.ldk + i] = (int8_t)d1;
-    b0[2 * D.ldk + i] = (int8_t)d2;
-    b0[3 * D.ldk + i] = (int8_t)d3;
+    const int ix = bq_index(D, i);
+    b0[ix] = (int8_t)T;
+    b0[D.ldk + ix] = (int8_t)d1;
+    b0[2 * D.ldk + ix] = (int8_t)d2;
+    b0[3 * D.ldk + ix] = (int8_t)d3;
   }
   ts = block_sum_ll(ts, smll);
   if (threadIdx.x == 0) {
@@ -199,6 +200,156 @@ __global__ void __launch_bounds__(FT) k_finalize(const Dev D) {
   if (threadIdx.x == 0) {
     D.sup_cnt[par] = 0;
     *D.iter = k + 1;
+  }
+}
+
+// ---------------------------------------------------------------- multi-CTA finalize
+// Same arithmetic as k_finalize, one row per thread over ceil(n/256) CTAs.  Each CTA
+// quantises its rows of theta^{k+1} with the exponent of the previous iteration's
+// max|theta| (provisional); the last CTA to finish (ticket) reduces the partials in
+// CTA order, and only if the exponent of max|theta^{k+1}| differs does it
+// re-quantise every row, so the digit planes are always those of the exact rule
+// delta = 2^(e-28), e = exponent of max|theta^{k+1}| (as in quantize_theta).
+
+__device__ __forceinline__ long long quant_row(const Dev& D, int r, int i, double th, double inv) {
+  long long T = isfinite(th) ? __double2ll_rn(th * inv) : 0;
+  const long long Tr = T;
+  int8_t* b0 = D.Bq + (int64_t)(4 * r) * D.ldk;
+  const int d3 = (int)(int8_t)(T & 0xFF);
+  T = (T - d3) >> 8;
+  const int d2 = (int)(int8_t)(T & 0xFF);
+  T = (T - d2) >> 8;
+  const int d1 = (int)(int8_t)(T & 0xFF);
+  T = (T - d1) >> 8;
+  const int ix = bq_index(D, i);
+  b0[ix] = (int8_t)T;
+  b0[D.ldk + ix] = (int8_t)d1;
+  b0[2 * D.ldk + ix] = (int8_t)d2;
+  b0[3 * D.ldk + ix] = (int8_t)d3;
+  return Tr;
+}
+
+__device__ __forceinline__ int theta_exponent(double mx) {
+  int ex = 0;
+  if (mx > 0.0 && isfinite(mx)) frexp(mx, &ex);
+  return ex;
+}
+
+__global__ void __launch_bounds__(FIN_THREADS) k_finalize_mc(const Dev D) {
+  __shared__ double smd[32 * 8 + 8];
+  __shared__ long long smll[33];
+  __shared__ bool s_last;
+  if (*D.stop) return;
+  const long long k = *D.iter;
+  const int par = (int)(k & 1), par1 = par ^ 1;
+  const int n = D.n;
+  const int i = blockIdx.x * FIN_THREADS + threadIdx.x;
+  for (int r = 0; r < D.R; ++r) {
+    if (D.status[r] != ST_ACTIVE) continue;
+    const double b0 = D.beta[par][r] + D.sumth[r] / D.eta[0];   // E14 with lambda_0 = 0, g_0 = sum theta^k
+    const double tau = D.tau[r];
+    const double mu = D.mu, sig = D.sigma;
+    const double tn = tau / ((double)n * mu), un = (1.0 - tau) / ((double)n * mu);
+    const int cnt = D.sup_cnt[par1];
+    const double cm = __longlong_as_double((long long)D.cmax[par1 * D.R + r]);
+    const int E = fwd_exponent(cm, cnt, n);
+    const long long mt = D.mterm[r];
+    const double inv_scale = ldexp(1.0, -E);
+    const double inv_prev = 1.0 / D.delta[r];   // 1/delta^k, exact (a power of two)
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long ts = 0;
+    if (i < n) {
+      const int64_t o = (int64_t)r * n + i;
+      const double sv = (double)((long long)n * D.sacc[o] - mt) * inv_scale / (double)n + b0;
+      D.sacc[o] = 0;
+      const double yi = D.y[i];
+      const double zo = D.z[o], th = D.theta[o], ro = D.rres[o];
+      const double zn = pos_part(zo + th / mu - tn) - pos_part(-zo - th / mu - un);   // E15
+      const double rn = sv + zn - yi;
+      const double thn = th - sig * (2.0 * rn - ro);                                  // E12
+      D.z[o] = zn;
+      D.theta[o] = thn;
+      D.rres[o] = rn;
+      D.s[o] = sv;
+      const double nt = (double)n * thn;
+      const double dz = zn - prox_rho1(zn + nt, tau);
+      acc[0] = rn * rn;
+      acc[1] = zn * zn;
+      acc[2] = nt * nt;
+      acc[3] = dz * dz;
+      acc[4] = rho_tau(yi - sv, tau);
+      acc[5] = thn;
+      acc[6] = yi * yi;
+      acc[7] = isfinite(thn) ? fabs(thn) : thn;
+      ts = quant_row(D, r, i, thn, inv_prev);
+    }
+    block_sum<7>(*(double(*)[7])acc, smd);
+    const double mx = block_max(acc[7], smd);
+    ts = block_sum_ll(ts, smll);
+    if (threadIdx.x == 0) {
+      double* fp = D.fpart + ((size_t)blockIdx.x * D.R + r) * FSQR_FPART;
+      for (int q = 0; q < 7; ++q) fp[q] = acc[q];
+      fp[7] = mx;
+      D.ftsum[(size_t)blockIdx.x * D.R + r] = ts;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(D.fticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // ------------------------------------------------ last CTA: fixed-order reduction over CTAs
+  for (int r = 0; r < D.R; ++r) {
+    if (D.status[r] != ST_ACTIVE) continue;
+    __shared__ double s_mx;
+    __shared__ int s_requant;
+    double a[7];
+    reduce_records<7>(D.fpart + (size_t)r * FSQR_FPART, (int)gridDim.x, D.R * FSQR_FPART, a, smd);
+    double mxl = 0.0;
+    long long tsl = 0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += FIN_THREADS) {
+      const double m = D.fpart[((size_t)b * D.R + r) * FSQR_FPART + 7];
+      mxl = (m > mxl || !isfinite(m)) ? m : mxl;
+      tsl += D.ftsum[(size_t)b * D.R + r];
+    }
+    const double mx = block_max(mxl, smd);
+    const long long ts = block_sum_ll(tsl, smll);
+    if (threadIdx.x == 0) {
+      double* sc = D.scal + r * FSQR_NSCAL;
+      sc[0] = sqrt(a[0]) / (1.0 + sqrt(a[6]));
+      sc[1] = sqrt(a[3]) / (1.0 + sqrt(a[1]) + sqrt(a[2]));
+      sc[2] = a[4];
+      sc[3] = a[6];
+      const double b0 = D.beta[par][r] + D.sumth[r] / D.eta[0];
+      D.beta[par1][r] = b0;
+      D.sumth[r] = a[5];
+      D.mterm[r] = 0;
+      const int e_new = theta_exponent(mx);
+      const int e_old = theta_exponent(D.delta[r] * ldexp(1.0, 28) * 0.75);   // delta^k = 2^(e_old - 28)
+      s_requant = (e_new != e_old) ? 1 : 0;
+      const double dlt = (mx > 0.0 && isfinite(mx)) ? ldexp(1.0, e_new - 28) : 1.0;
+      s_mx = dlt;
+      if (!s_requant) {
+        D.Tsum[r] = ts;
+      }
+      D.delta[r] = dlt;
+    }
+    __syncthreads();
+    if (s_requant) {
+      const double inv = 1.0 / s_mx;
+      long long ts = 0;
+      for (int ii = threadIdx.x; ii < n; ii += FIN_THREADS) ts += quant_row(D, r, ii, D.theta[(int64_t)r * n + ii], inv);
+      ts = block_sum_ll(ts, smll);
+      if (threadIdx.x == 0) D.Tsum[r] = ts;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < D.R) D.cmax[par * D.R + threadIdx.x] = 0ull;
+  if (threadIdx.x == 0) {
+    D.sup_cnt[par] = 0;
+    *D.iter = k + 1;
+    *D.fticket = 0u;
   }
 }
 
@@ -448,27 +599,66 @@ __global__ void k_build_support(const Dev D, int par) {
 // penalty of the committed beta and original-scale conversion (one CTA, fixed order)
 __global__ void __launch_bounds__(FT) k_commit_stats(const Dev D, double* pen_out /*[R]*/, double* beta_out /*[R][p+1] or null*/,
                                                      int orig) {
-  __shared__ double smd[32 * 2 + 2];
+  __shared__ double smd[32 * 3 + 3];
   const long long k = *D.iter;
+  const bool use_w = *D.use_w != 0;
   for (int r = 0; r < D.R; ++r) {
     const long long ci = D.status[r] == ST_ACTIVE ? k : D.commit_iter[r];
     const double* beta = D.beta[(int)(ci & 1)];
-    double a[2] = {0.0, 0.0};
+    double a[3] = {0.0, 0.0, 0.0};
     for (int64_t j = 1 + threadIdx.x; j <= D.p; j += blockDim.x) {
       const double b = beta[j * D.R + r];
-      const double w = D.lamw ? D.lamw[j] : 1.0;
-      a[0] += D.lam_cur[r] * w * fabs(b);
+      const double lam = use_w ? D.lam_cur[r] * D.lamw[j * D.R + r] : D.lam_cur[r];
+      a[0] += lam * fabs(b);
       const double bo = b * D.inv_sd[j - 1];
       a[1] += D.mean[j - 1] * bo;
+      a[2] += b != 0.0 ? 1.0 : 0.0;
       if (beta_out) beta_out[(int64_t)r * (D.p + 1) + j] = orig ? bo : b;
     }
-    block_sum<2>(a, smd);
+    block_sum<3>(a, smd);
     if (threadIdx.x == 0) {
-      if (pen_out) pen_out[r] = a[0];
+      if (pen_out) {
+        pen_out[r] = a[0];
+        pen_out[D.R + r] = a[2];   // |A|: nonzero penalised coefficients
+      }
       if (beta_out) beta_out[(int64_t)r * (D.p + 1)] = orig ? beta[r] - a[1] : beta[r];
     }
     __syncthreads();
   }
+}
+
+// Algorithm 2: w_jr = p'_lam_r(|beta~_jr|) / lam_r from the committed beta,
+// SCAD (kind 1, E16 L354-361) or MCP (kind 2, E17 L363-369); the intercept is never penalised.
+__global__ void k_lla_weights(const Dev D, int kind, double a) {
+  const long long k = *D.iter;
+  for (int r = 0; r < D.R; ++r) {
+    const long long ci = D.status[r] == ST_ACTIVE ? k : D.commit_iter[r];
+    const double* beta = D.beta[(int)(ci & 1)];
+    const double lam = D.lam_cur[r];
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= D.p; j += (int64_t)gridDim.x * blockDim.x) {
+      double w = 0.0;
+      if (j > 0) {
+        const double ab = fabs(beta[j * D.R + r]);
+        double d;
+        if (kind == 1) d = ab <= lam ? lam : (ab < a * lam ? (a * lam - ab) / (a - 1.0) : 0.0);
+        else d = ab <= a * lam ? lam - ab / a : 0.0;
+        w = d / lam;
+      }
+      D.lamw[j * D.R + r] = w;
+    }
+  }
+}
+
+// resume after a stop: the K2 pass that detected convergence at iteration k had already appended
+// beta^{k+1} to the support list of parity k+1 (and raised its cmax) before K1/finalize were
+// skipped; that list must be empty again before iteration k is re-run.
+__global__ void k_resume(const Dev D) {
+  const int par1 = (int)((*D.iter + 1) & 1);
+  if (threadIdx.x == 0) {
+    D.sup_cnt[par1] = 0;
+    *D.kbase = *D.iter;
+  }
+  if (threadIdx.x < D.R) D.cmax[par1 * D.R + threadIdx.x] = 0ull;
 }
 
 // resume after a solve froze some RHS: bring their committed beta into the current parity buffer
@@ -486,7 +676,12 @@ __global__ void k_unfreeze(const Dev D) {
 
 }  // namespace
 
-void launch_finalize(const Dev& D, cudaStream_t st) { k_finalize<<<1, FT, 0, st>>>(D); }
+void launch_finalize(const Dev& D, cudaStream_t st) {
+  if (D.storage == 0)
+    k_finalize<<<1, FT, 0, st>>>(D);
+  else
+    k_finalize_mc<<<(D.n + FIN_THREADS - 1) / FIN_THREADS, FIN_THREADS, 0, st>>>(D);
+}
 void launch_init_state(const Dev& D, cudaStream_t st) { k_init_state<<<1, FT, 0, st>>>(D); }
 void launch_colstats(const Dev& D, int32_t* colsum, double* mean, double* inv_sd, double* sd, int* bad,
                      cudaStream_t st) {
@@ -524,4 +719,10 @@ void launch_build_support(const Dev& D, int par, cudaStream_t st) {
 void launch_commit_stats(const Dev& D, double* pen, double* beta_out, int orig, cudaStream_t st) {
   k_commit_stats<<<1, FT, 0, st>>>(D, pen, beta_out, orig);
 }
-void launch_unfreeze(const Dev& D, cudaStream_t st) { k_unfreeze<<<256, 256, 0, st>>>(D); }
+void launch_unfreeze(const Dev& D, cudaStream_t st) {
+  k_resume<<<1, 32, 0, st>>>(D);
+  k_unfreeze<<<256, 256, 0, st>>>(D);
+}
+void launch_lla_weights(const Dev& D, int kind, double a, cudaStream_t st) {
+  k_lla_weights<<<592, 256, 0, st>>>(D, kind, a);
+}

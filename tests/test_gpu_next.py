@@ -1,0 +1,102 @@
+"""GPU parity for SURVEY §8(f) NEXT #1-#2 built on the hot path: per-coefficient penalty weights
+(weighted l1, E4), the L-step LLA for SCAD / MCP (Algorithm 2) and HBIC (E18,
+L408-411).  Expected values come from the fp64 oracle on the same seeded inputs."""
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+from gpu_helpers import rel, to_device
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(n=800, p=2000, tau=0.5, lam_frac=0.1, storage=None, name="c2", tol=1e-6):
+    import paper_2601_02826_b200 as fs
+
+    prob = datagen.make(name, n=n, p=p, storage=storage)
+    d = oracle.Design.from_problem(prob)
+    mu, G = 2.0 / prob.n, 5
+    eta = oracle.eta(d, G, mu)
+    lam = lam_frac * oracle.lambda_max(d, prob.y, tau)[0]
+    X, y = to_device(prob)
+    S = fs.Solver(X, prob.storage, prob.n, prob.p, prob.ld, y, [tau], [lam], G=G, mu=mu, eta=eta, tol=tol,
+                  max_iter=200000)
+    return prob, d, S, dict(mu=mu, G=G, eta=eta, lam=lam, tau=tau)
+
+
+def test_weighted_l1_fixed_iterations(cuda_ok):
+    """Random non-negative weights (a tenth of them zero: unpenalised coefficients)."""
+    prob, d, S, c = _setup()
+    rng = np.random.default_rng(5)
+    w = rng.uniform(0.2, 3.0, prob.p + 1)
+    w[rng.choice(prob.p, prob.p // 10, replace=False) + 1] = 0.0
+    S.set_lambda_weights(w[None, :])
+    S.iterate(150)
+    b, z, t = S.state()
+    lv = oracle.lam_vector(prob.p, c["lam"], w)
+    o = oracle.solve(d, prob.y, c["tau"], lv, c["eta"], c["mu"], c["G"], max_iter=150, check=False)
+    assert rel(b[0], o["beta"]) < 1e-6
+    assert rel(t[0], o["theta"]) < 1e-6
+    assert np.array_equal(b[0] != 0, o["beta"] != 0)
+    assert S.objective()[0] == pytest.approx(oracle.objective(d, prob.y, c["tau"], lv, o["beta"]), rel=1e-6)
+    # unit weights restored: identical to a fresh unweighted run of the same length from this state
+    S.set_lambda_weights(None)
+
+
+@pytest.mark.parametrize("kind,a", [(1, 3.7), (2, 3.0)])
+def test_one_step_lla_matches_oracle(cuda_ok, kind, a):
+    """The paper's protocol (one-step LLA, a = 3.7 SCAD / 3 MCP, L404) on the C2 recipe at reduced
+    size: per-stage iteration counts, the final beta, support and weighted objective agree."""
+    prob, d, S, c = _setup(storage=None)
+    res = S.lla(kind, a, 1)
+    assert res["status"] == 0, res
+    o = oracle.lla(d, prob.y, c["tau"], c["lam"], kind, a, 1, c["eta"], c["mu"], c["G"], tol=1e-6, max_iter=200000)
+    for l, st in enumerate(o["stages"]):
+        assert st["status"] == 0
+        assert abs(res["stage_iters"][l] - st["iters"]) <= 2, (l, res["stage_iters"], [s["iters"] for s in o["stages"]])
+    b = S.beta()[0]
+    assert rel(b, o["beta"]) < 1e-4
+    assert np.array_equal(b != 0, o["beta"] != 0)
+    lv = oracle.lam_vector(prob.p, c["lam"], o["stages"][-1]["weights"])
+    assert S.objective()[0] == pytest.approx(oracle.objective(d, prob.y, c["tau"], lv, o["beta"]), rel=1e-4)
+    # the stage-1 weights of the largest LASSO coefficients are below 1 (less shrinkage, L352)
+    w1 = o["stages"][1]["weights"]
+    big = np.argmax(np.abs(o["stages"][0]["beta"][1:])) + 1
+    assert w1[big] < 1.0
+
+
+def test_lla_on_two_bit_storage(cuda_ok):
+    """Same driver on the 2-bit packed storage (C4 recipe, tensor-core kernel), MCP, L = 2."""
+    prob, d, S, c = _setup(name="c4", n=700, p=1500, storage=2)
+    assert S.backend == "tc"
+    res = S.lla(2, 3.0, 2)
+    assert res["status"] == 0
+    o = oracle.lla(d, prob.y, c["tau"], c["lam"], 2, 3.0, 2, c["eta"], c["mu"], c["G"], tol=1e-6, max_iter=200000)
+    assert rel(S.beta()[0], o["beta"]) < 1e-4
+    assert np.array_equal(S.beta()[0] != 0, o["beta"] != 0)
+
+
+def test_hbic_matches_oracle(cuda_ok):
+    prob, d, S, c = _setup(tau=0.3)
+    res = S.solve()
+    assert res["status"] == 0
+    o = oracle.solve(d, prob.y, c["tau"], oracle.lam_vector(prob.p, c["lam"]), c["eta"], c["mu"], c["G"],
+                     max_iter=200000, tol=1e-6)
+    h = S.hbic()[0]
+    ho = oracle.hbic(d, prob.y, c["tau"], o["beta"])
+    assert h == pytest.approx(ho, rel=1e-6)
+
+
+def test_lla_bad_arguments(cuda_ok):
+    import paper_2601_02826_b200 as fs
+
+    prob, d, S, c = _setup(n=200, p=300)
+    for args in ((3, 3.7, 1), (1, 1.5, 1), (2, 0.9, 1), (1, 3.7, -1)):
+        with pytest.raises(fs.FsqrError) as e:
+            S.lla(*args)
+        assert e.value.status == -1
+    bad = np.ones((1, prob.p + 1))
+    bad[0, 3] = -1.0
+    with pytest.raises(fs.FsqrError):
+        S.set_lambda_weights(bad)

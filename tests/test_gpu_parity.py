@@ -38,6 +38,8 @@ def test_colstats_lambda_max_eta(cuda_ok):
     ("c2", 1, 1000, 3001, 1),         # u8, tcgen05: ragged K tail (1000 % 128) and column tail (3001 % 128)
     ("c2", 1, 1000, 3001, 2),         # u8, dp4a
     ("c4", 2, 999, 2050, 2),          # 2-bit packed, dp4a
+    ("c4", 2, 999, 2050, 1),          # 2-bit packed, tcgen05 with the unpacked A operand in TMEM
+    ("c4", 2, 1537, 700, 1),          # 2-bit tcgen05: n just past a 512-sample K block
 ])
 def test_fixed_iterations(cuda_ok, name, storage, n, p, backend):
     prob, d, S, cfg = make_pair(name, n=n, p=p, storage=storage, backend=backend, taus=[0.5])
@@ -59,17 +61,24 @@ def test_fixed_iterations(cuda_ok, name, storage, n, p, backend):
         assert obj == pytest.approx(oo, rel=1e-4)
 
 
-def test_tc_equals_simt_bitwise(cuda_ok):
-    """Both X~^T theta kernels reduce the same exact integers: beta must agree bit for bit."""
+@pytest.mark.parametrize("name,storage,taus", [
+    ("c2", 1, [0.5]),
+    ("c4", 2, [0.5]),
+    ("c4", 2, [0.2, 0.5, 0.8]),
+    ("c4", 2, [0.1 * (i + 1) for i in range(9)]),
+])
+def test_tc_equals_simt_bitwise(cuda_ok, name, storage, taus):
+    """Both X~^T theta kernels reduce the same exact integers: beta must agree bit for bit
+    (u8 and 2-bit tensor-core kernels against the dp4a kernel, 1, 3 and 9 RHS)."""
     import paper_2601_02826_b200 as fs
 
-    prob = datagen.make("c2", n=1500, p=5000)
+    prob = datagen.make(name, n=1500, p=5000, storage=storage)
     d = oracle.Design.from_problem(prob)
-    lm, _ = oracle.lambda_max(d, prob.y, 0.5)
+    lams = [0.05 * oracle.lambda_max(d, prob.y, t)[0] for t in taus]
     X, y = to_device(prob)
     out = []
     for be in (fs.BACKEND_TC, fs.BACKEND_SIMT):
-        S = fs.Solver(X, 1, prob.n, prob.p, prob.ld, y, [0.5], [0.05 * lm], G=5, backend=be, eta=[40.0] * 5)
+        S = fs.Solver(X, storage, prob.n, prob.p, prob.ld, y, taus, lams, G=5, backend=be, eta=[40.0] * 5)
         assert S.backend == ("tc" if be == fs.BACKEND_TC else "simt")
         S.iterate(60)
         out.append(S.state())

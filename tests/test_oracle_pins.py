@@ -336,3 +336,76 @@ def test_path_warm_start_semantics():
                             max_iter=300000, tol=1e-9)
         assert cold["status"] == 0
         assert res["obj"][t] == pytest.approx(cold["obj"], rel=1e-6)
+
+
+# ----------------------------------------------------------------- Section 5 (LLA) and HBIC pins
+
+@pytest.mark.parametrize("case", GOLD["penalty_deriv"])
+def test_penalty_deriv_worked_values(case):
+    assert oracle.penalty_deriv(case["kind"], case["a"], case["lam"], case["b"]) == pytest.approx(case["expect"],
+                                                                                                 abs=1e-15)
+
+
+@pytest.mark.parametrize("kind,a", [(oracle.SCAD, 3.7), (oracle.SCAD, 2.5), (oracle.MCP, 3.0), (oracle.MCP, 1.5)])
+def test_penalty_deriv_shape(kind, a):
+    """E16/E17: continuous at the knots, even in b, non-increasing in |b|, lam at 0, 0 beyond a*lam."""
+    lam = 0.8
+    b = np.linspace(0, 1.2 * a * lam, 2001)
+    d = np.array([oracle.penalty_deriv(kind, a, lam, v) for v in b])
+    assert d[0] == pytest.approx(lam)
+    assert np.all(np.diff(d) <= 1e-15)
+    assert np.all(d >= 0) and d[-1] == 0.0
+    assert np.max(np.abs(np.diff(d))) < 2 * lam * (b[1] - b[0]) / min(a - 1.0, 1.0) + 1e-12   # no jumps
+    for v in (0.3, 1.1, 2.9):
+        assert oracle.penalty_deriv(kind, a, lam, -v) == oracle.penalty_deriv(kind, a, lam, v)
+    w = oracle.lla_weights(kind, a, lam, np.array([5.0, 0.0, 0.5 * lam, -10 * a * lam]))
+    assert w[0] == 0.0 and w[1] == 1.0 and w[3] == 0.0
+
+
+@pytest.mark.parametrize("case", GOLD["hbic"])
+def test_hbic_worked_value(case):
+    v = oracle.hbic_value(case["loss"], case["active"], case["n"], case["p"])
+    assert v == pytest.approx(case["expect"], abs=case["tol"])
+
+
+def test_hbic_null_model_closed_form():
+    prob = datagen.make("c2", n=50, p=8, seed=31)
+    d = oracle.Design.from_problem(prob)
+    beta = np.zeros(prob.p + 1)
+    beta[0] = np.median(prob.y)
+    loss = np.sum(np.where(prob.y - beta[0] < 0, -0.5 * (prob.y - beta[0]), 0.5 * (prob.y - beta[0])))
+    assert oracle.hbic(d, prob.y, 0.5, beta) == pytest.approx(np.log(loss), rel=1e-12)
+    beta[[2, 5]] = [0.1, -0.2]
+    act_term = 2 * np.log(np.log(50)) / 50 * np.log(8)
+    A, _, _ = _np_standardized(prob)
+    u = prob.y - A @ beta
+    loss2 = np.sum(np.where(u < 0, -0.5 * u, 0.5 * u))
+    assert oracle.hbic(d, prob.y, 0.5, beta) == pytest.approx(np.log(loss2) + act_term, rel=1e-10)
+
+
+@pytest.mark.parametrize("kind,a,seed", [(oracle.SCAD, 3.7, 41), (oracle.MCP, 3.0, 42)])
+def test_lla_stages_are_weighted_l1_optima(kind, a, seed):
+    """Algorithm 2: every stage l is the weighted-l1 PQR with lam_j = p'_lam(|beta~^{l-1}_j|); its
+    converged objective equals the exact optimum of that weighted problem (vertex enumeration)."""
+    prob, d = _tiny(seed, n=14, p=3)
+    A, _, _ = _np_standardized(prob)
+    tau = 0.5
+    lm, _ = oracle.lambda_max(d, prob.y, tau)
+    lam = 0.4 * lm
+    G, mu = 2, 0.1
+    eta = oracle.eta(d, G, mu)
+    out = oracle.lla(d, prob.y, tau, lam, kind, a, 2, eta, mu, G, tol=1e-11, max_iter=400000)
+    assert len(out["stages"]) == 3
+    prev = None
+    for l, st in enumerate(out["stages"]):
+        assert st["status"] == 0
+        if l == 0:
+            assert np.all(st["weights"][1:] == 1.0)
+        else:
+            np.testing.assert_array_equal(st["weights"], oracle.lla_weights(kind, a, lam, prev))
+        lv = oracle.lam_vector(prob.p, lam, st["weights"])
+        fstar, _ = lp.vertex_enumeration(A, prob.y, tau, lv)
+        assert st["obj"] == pytest.approx(fstar, rel=1e-8, abs=1e-12)
+        prev = st["beta"]
+    # the concave penalty lightens the shrinkage of large coefficients: stage weights <= 1
+    assert np.all(out["stages"][1]["weights"] <= 1.0)
