@@ -33,13 +33,17 @@ constexpr int TILE_M = 128;               // columns per tile (UMMA M)
 constexpr int PK = 128;                   // packed bytes per column per stage
 constexpr int KS = 4 * PK;                // samples (K) per stage
 constexpr int A_BYTES = TILE_M * PK;      // 16 KB packed A per stage
-constexpr int THREADS = 384;              // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-7 convert, w8-11 epilogue
 constexpr int NAB = 3;                    // TMEM A buffers
 constexpr int A_COLS = KS / 4;            // TMEM columns per A buffer (4 int8 per 32-bit cell)
 constexpr int A_COL0 = 128;               // A buffers start after the accumulators (2*NPAD <= 128)
 
+// warps: 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4..4+CW-1 convert, then 4 epilogue warps.  One RHS
+// (the C4 workload) keeps few registers per thread, so it affords 8 converter warps (two per SM
+// sub-partition: the unpack loop is latency-bound with one); more RHS keep 4.
 template <int NPAD, int RM>
 struct Cfg2 {
+  static constexpr int CW = RM == 1 ? 8 : 4;
+  static constexpr int THREADS = 32 * (8 + CW);
   static constexpr int B_ATOM = NPAD * 128;
   static constexpr int B_BYTES = 4 * B_ATOM;
   static constexpr int STAGE = A_BYTES + B_BYTES;
@@ -70,13 +74,24 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
       "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 template <int NPAD, int RM>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
     k2_tc2_kernel(const Dev D, const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmB) {
   using CF = Cfg2<NPAD, RM>;
   constexpr int RMAX = CF::RMAX;
+  constexpr int CW = CF::CW;
+  constexpr int THREADS = CF::THREADS;
+  constexpr int EPI0 = 4 + CW;   // first epilogue warp
   if (*D.stop) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -108,7 +123,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < NAB; ++a) {
-      mbar_init(&afull[a], 4);
+      mbar_init(&afull[a], CW);
       mbar_init(&aempty[a], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -209,9 +224,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         __syncwarp();
       }
     }
-  } else if (wid >= 4 && wid < 8) {
-    // ===== converters: thread = tile column 32*(wid-4) + lane = TMEM lane =====
-    const int q4 = wid - 4;
+  } else if (wid >= 4 && wid < EPI0) {
+    // ===== converters: TMEM lane quarter wid % 4 (thread = tile column), column half h of the
+    // packed row when CW = 8 =====
+    constexpr int CH = 8 / (CW / 4);          // 16-byte chunks per converter thread (8 or 4)
+    constexpr int NW = 4 * CH;                // packed words per thread
+    const int q4 = wid & 3;
+    const int h = (wid - 4) >> 2;             // 0 (CW = 4) or 0/1 (CW = 8)
     const int c = q4 * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     int stage = 0, ab = 0;
@@ -221,23 +240,25 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(&full[stage], phase);
         mbar_wait(&aempty[ab], aphase ^ 1);
         tc_fence_after();
-        uint32_t w[32];
+        uint32_t w[NW];
         const uint8_t* row = sA + stage * A_BYTES + c * PK;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {   // logical 16-byte chunk j sits at chunk j ^ (c & 7) (SWIZZLE_128B)
+        for (int jj = 0; jj < CH; ++jj) {   // logical 16-byte chunk j sits at chunk j ^ (c & 7) (SWIZZLE_128B)
+          const int j = h * CH + jj;
           const uint4 v = *(const uint4*)(row + ((j ^ (c & 7)) << 4));
-          w[4 * j] = v.x;
-          w[4 * j + 1] = v.y;
-          w[4 * j + 2] = v.z;
-          w[4 * j + 3] = v.w;
+          w[4 * jj] = v.x;
+          w[4 * jj + 1] = v.y;
+          w[4 * jj + 2] = v.z;
+          w[4 * jj + 3] = v.w;
         }
-        const uint32_t abase = tmem_base + lane_off + (uint32_t)(A_COL0 + ab * A_COLS);
+        const uint32_t abase = tmem_base + lane_off + (uint32_t)(A_COL0 + ab * A_COLS + h * NW);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          uint32_t o[32];
+          uint32_t o[NW];
 #pragma unroll
-          for (int u = 0; u < 32; ++u) o[u] = (w[u] >> (2 * q)) & 0x03030303u;
-          tmem_st32(abase + (uint32_t)(32 * q), o);
+          for (int u = 0; u < NW; ++u) o[u] = (w[u] >> (2 * q)) & 0x03030303u;
+          if constexpr (NW == 32) tmem_st32(abase + (uint32_t)(32 * q), o);
+          else tmem_st16(abase + (uint32_t)(32 * q), o);
         }
         tmem_wait_st();
         tc_fence_before();
@@ -253,9 +274,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
-  } else if (wid >= 8) {
-    // ===== epilogue: TMEM lanes 32*(wid-8) .. +31 = columns of the tile =====
-    const int q = wid - 8;
+  } else if (wid >= EPI0) {
+    // ===== epilogue: TMEM lanes 32*(wid%4) .. +31 = columns of the tile =====
+    const int q = wid & 3;
     int lt = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
       const int acc = lt & 1;
@@ -304,7 +325,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 template <int NPAD, int RM>
 void launch_np(const Dev& D, const void* tmX, const void* tmB, int grid, cudaStream_t st) {
-  k2_tc2_kernel<NPAD, RM><<<grid, THREADS, Cfg2<NPAD, RM>::SMEM, st>>>(D, *(const CUtensorMap*)tmX,
+  k2_tc2_kernel<NPAD, RM><<<grid, Cfg2<NPAD, RM>::THREADS, Cfg2<NPAD, RM>::SMEM, st>>>(D, *(const CUtensorMap*)tmX,
                                                                 *(const CUtensorMap*)tmB);
 }
 
