@@ -33,6 +33,7 @@ sys.path.insert(0, ROOT)
 
 import datagen  # noqa: E402
 
+STATUS_NAMES = {0: "converged", 2: "max_iter"}
 METRIC = "PPA iters/sec and X-streaming HBM GB/s (% of peak) at n=10k, p=1M, tau=0.5"
 FALLBACK_HBM = 6650.0
 
@@ -217,7 +218,8 @@ def run_ours(args):
 
     # setup (a0, a0', lambda_max) timed separately; lambda = frac * lambda_max from the GPU
     t0 = time.perf_counter()
-    S = fs.Solver(Xd, prob.storage, prob.n, prob.p, prob.ld, yd, [tau], [1.0], G=G, mu=mu)
+    S = fs.Solver(Xd, prob.storage, prob.n, prob.p, prob.ld, yd, [tau], [1.0], G=G, mu=mu, tol=args.kkt_tol,
+                  max_iter=args.kkt_max_iter)
     lm = float(S.lambda_max()[0])
     S.set_lambda([prob.lam_frac * lm])
     t_setup = time.perf_counter() - t0
@@ -272,6 +274,20 @@ def run_ours(args):
                "note": "one fsqr_fit_host call: H2D of X,y (pinned) + setup (eta given) + k iterations + D2H beta"}
         del Xp
 
+    # time to KKT tolerance: fsqr_solve from the cold start (beta=0, z=y, theta=0),
+    # device time of the whole solve (graph chunks, device-side stopping test)
+    kkt = None
+    if not args.no_kkt:
+        S.set_state(np.zeros((1, prob.p + 1)), prob.y[None, :], np.zeros((1, prob.n)))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = S.solve()
+        wall = time.perf_counter() - t0
+        kkt = {"tol": args.kkt_tol, "status": STATUS_NAMES.get(res["status"], res["status"]),
+               "iterations": int(res["iterations"]), "device_s": res["wall_ms"] / 1000.0, "wall_s": wall,
+               "R": [float(v) for v in res["R"][0]], "objective": float(res["objective"][0]),
+               "support": int(S.trace(1)[-1, 0, 4])}
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         cpu = cpu_baseline(prob, prob.lam_frac, tau, G, mu)
@@ -293,6 +309,7 @@ def run_ours(args):
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "time_to_kkt": kkt,
             "gpu_launches": 3 * k,
             "clocks": clocks,
         }
@@ -312,6 +329,9 @@ def main():
     ap.add_argument("--burn-in", dest="burn_in", type=int, default=200)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-kkt", action="store_true")
+    ap.add_argument("--kkt-tol", dest="kkt_tol", type=float, default=1e-4)
+    ap.add_argument("--kkt-max-iter", dest="kkt_max_iter", type=int, default=30000)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

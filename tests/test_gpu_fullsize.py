@@ -109,7 +109,10 @@ def check_one_step(prob, S, taus, lams, eta, mu, G, seed=7, ncols=4000):
         r0 = s0 + z0[r] - prob.y
         r1 = s1 + z1[r] - prob.y
         dth = -sigma * (2 * r1 - r0)
-        assert rel(t1[r] - t0[r], dth) < 1e-6
+        # E12 consumes the forward products s^k, s^{k+1}: with those within north_star's product
+        # tolerance (1e-5 relative) the dual step can differ by at most sigma (2 |ds1| + |ds0|)
+        err = np.linalg.norm((t1[r] - t0[r]) - dth)
+        assert err <= 1e-5 * sigma * (2 * np.linalg.norm(s1) + np.linalg.norm(s0)), (err, np.linalg.norm(dth))
     return n_checked, len(sup)
 
 
