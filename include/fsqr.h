@@ -164,6 +164,17 @@ fsqr_status fsqr_set_lambda_weights(fsqr_ctx* ctx, const double* w_host, void* s
 fsqr_status fsqr_lla(fsqr_ctx* ctx, int32_t penalty, double a, int32_t L, int64_t* stage_iters_host,
                      fsqr_result* out, void* stream);
 
+/*
+ * Pivotal statistic for the lambda grid ("the pivotal quantity approach"; App. F is
+ * missing, reading R18): for Monte-Carlo replicates b = 0..B-1 with uniforms
+ * U_bi = top 53 bits of splitmix64(seed ^ splitmix64((b << 32) | i)),
+ *     Lambda_host[b] = max_{j>=1} | sum_i x~_ij (tau_rhs - 1{U_bi <= tau_rhs}) | / n.
+ * 128 replicates per pass over X on the tensor cores (exact integer sums).  The conventional
+ * choice is lambda = 1.1 x the 0.9 empirical quantile of Lambda (Belloni-Chernozhukov).
+ * U8 storage only (else FSQR_ERR_CONFIG).  Blocking.
+ */
+fsqr_status fsqr_pivotal(fsqr_ctx* ctx, int32_t rhs, int64_t B, uint64_t seed, double* Lambda_host, void* stream);
+
 /* beta of the committed iterate, [n_rhs][p+1] row per RHS.
  * scale 0: standardised; scale 1: original scale, beta_j/s_j and beta_0 - sum m_j beta_j/s_j (L404). */
 fsqr_status fsqr_get_beta(fsqr_ctx* ctx, double* beta_host, int32_t scale, void* stream);

@@ -20,6 +20,9 @@ Parity status per function (DESIGN.md §4 repeats this table):
   penalty_deriv   pinned: SPEC worked values (SCAD, MCP), continuity at the knots, the LASSO limit
   lla             pinned: each stage is a weighted-l1 PQR whose optimum matches the LP brute force
                   with the stage's weights; Prop. 1 certificate per stage
+  pivotal         pinned: splitmix64 reference outputs, Bernoulli(tau) frequencies of the draws,
+                  E[(x~_j^T psi)^2] = tau(1-tau)(n-1) (law of large numbers), invariance to
+                  genotype recoding 2-x and to column order; a hand-built 3x2 case
   hbic            pinned: SPEC worked value and the closed form on a null model
   trajectory after k iterations: parity unpinned beyond the composition of pinned steps
                   (the paper prints no iterates); see DESIGN.md §4.
@@ -101,6 +104,11 @@ def _load():
         lib.orc_hbic_value.argtypes = [D, I64, I64, I64]
         lib.orc_hbic.restype = D
         lib.orc_hbic.argtypes = [DP, P, D, P]
+        lib.orc_piv_uniform.restype = D
+        lib.orc_piv_uniform.argtypes = [U64, I64, I64]
+        lib.orc_splitmix.restype = U64
+        lib.orc_splitmix.argtypes = [U64]
+        lib.orc_pivotal.argtypes = [DP, D, I64, U64, P]
         lib.orc_path.restype = I64
         lib.orc_path.argtypes = [DP, P, D, D, I32, P, P, P, I32, D, I64, P, P, P, P, P, P, P, P]
         _lib = lib
@@ -329,3 +337,26 @@ def hbic_value(loss: float, active: int, n: int, p: int) -> float:
 def hbic(d: Design, y, tau: float, beta) -> float:
     """HBIC (E18, L408-411) with C_n = log p."""
     return _load().orc_hbic(d.ref, _p(_f64(y)), float(tau), _p(_f64(beta)))
+
+
+def splitmix(x: int) -> int:
+    """One splitmix64 output for state x (x + golden gamma, then the finaliser)."""
+    return int(_load().orc_splitmix(int(x) & 0xFFFFFFFFFFFFFFFF))
+
+
+def piv_uniform(seed: int, b: int, i: int) -> float:
+    return _load().orc_piv_uniform(int(seed), int(b), int(i))
+
+
+def pivotal(d: Design, tau: float, B: int, seed: int = 0x5EED) -> np.ndarray:
+    """Lambda_b = max_j |sum_i x~_ij (tau - 1{U_ib <= tau})| / n, b < B (L412, reading R18)."""
+    out = np.empty(int(B))
+    _load().orc_pivotal(d.ref, float(tau), int(B), int(seed), _p(out))
+    return out
+
+
+def pivotal_lambda(Lambda, alpha: float = 0.1, c: float = 1.1) -> float:
+    """c times the (1-alpha) empirical quantile (order statistic ceil((1-alpha) B)) of Lambda_b."""
+    s = np.sort(np.asarray(Lambda, np.float64))
+    k = int(np.ceil((1.0 - alpha) * len(s)))
+    return float(c * s[max(k, 1) - 1])

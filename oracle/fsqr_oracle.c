@@ -543,3 +543,38 @@ double orc_hbic(const orc_design* X, const double* y, double tau, const double* 
   free(s);
   return orc_hbic_value(loss, act, n, X->p);
 }
+
+/* ------------------------------------------------ pivotal lambda (Section 6) */
+
+/*
+ * Uniform draw U_ib in [0, 1) of Monte-Carlo replicate b for observation i: the top 53 bits of
+ * splitmix64(seed ^ splitmix64((b << 32) | i)).  The CUDA path implements the same
+ * counter-based generator independently (shared definition, no shared code).
+ */
+double orc_piv_uniform(uint64_t seed, int64_t b, int64_t i) {
+  uint64_t h = orc_mix(seed ^ orc_mix(((uint64_t)b << 32) | (uint64_t)i));
+  return (double)(h >> 11) * 0x1.0p-53;
+}
+
+uint64_t orc_splitmix(uint64_t x) { return orc_mix(x); }
+
+/*
+ * Pivotal statistic of Belloni and Chernozhukov (the "pivotal quantity approach", L412; App. F
+ * missing, reading R18): for replicates b = 0..B-1,
+ *   Lambda_b = max_{j >= 1} | sum_i x~_ij (tau - 1{U_ib <= tau}) | / n.
+ * Written out directly: psi, then one X~^T psi per replicate.
+ */
+void orc_pivotal(const orc_design* X, double tau, int64_t B, uint64_t seed, double* Lambda) {
+  const int64_t n = X->n, p1 = X->p + 1;
+  double* psi = (double*)malloc(sizeof(double) * n);
+  double* g = (double*)malloc(sizeof(double) * p1);
+  for (int64_t b = 0; b < B; ++b) {
+    for (int64_t i = 0; i < n; ++i) psi[i] = tau - (orc_piv_uniform(seed, b, i) <= tau ? 1.0 : 0.0);
+    orc_backprod(X, psi, g);
+    double m = 0.0;
+    for (int64_t j = 1; j < p1; ++j) m = fmax(m, fabs(g[j]));
+    Lambda[b] = m / (double)n;
+  }
+  free(psi);
+  free(g);
+}

@@ -56,7 +56,7 @@ class fsqr_result(ctypes.Structure):
 EXPORTS = ["fsqr_default_options", "fsqr_create", "fsqr_iterate", "fsqr_solve", "fsqr_objective", "fsqr_kkt",
            "fsqr_get_beta", "fsqr_get_state", "fsqr_set_state", "fsqr_set_lambda", "fsqr_lambda_max",
            "fsqr_get_eta", "fsqr_get_colstats", "fsqr_path", "fsqr_path_beta", "fsqr_trace", "fsqr_iterations",
-           "fsqr_profile_iterate", "fsqr_hbic", "fsqr_set_lambda_weights", "fsqr_lla",
+           "fsqr_profile_iterate", "fsqr_hbic", "fsqr_set_lambda_weights", "fsqr_lla", "fsqr_pivotal",
            "fsqr_backend_name", "fsqr_fit_host", "fsqr_last_error", "fsqr_global_error", "fsqr_status_str",
            "fsqr_destroy"]
 
@@ -102,6 +102,7 @@ def load(build_if_missing: bool = True):
     L.fsqr_profile_iterate.argtypes = [ctxp, I64, P, P, P]
     L.fsqr_profile_iterate.restype = S
     L.fsqr_hbic.argtypes = [ctxp, P, P]
+    L.fsqr_pivotal.argtypes = [ctxp, I32, I64, ctypes.c_uint64, P, P]
     L.fsqr_set_lambda_weights.argtypes = [ctxp, P, P]
     L.fsqr_lla.argtypes = [ctxp, I32, D, I32, P, ctypes.POINTER(fsqr_result), P]
     L.fsqr_iterations.argtypes = [ctxp]
@@ -121,7 +122,7 @@ def load(build_if_missing: bool = True):
     for name in ("fsqr_create", "fsqr_iterate", "fsqr_solve", "fsqr_objective", "fsqr_kkt", "fsqr_get_beta",
                  "fsqr_get_state", "fsqr_set_state", "fsqr_set_lambda", "fsqr_lambda_max", "fsqr_get_eta",
                  "fsqr_get_colstats", "fsqr_path", "fsqr_path_beta", "fsqr_trace", "fsqr_fit_host", "fsqr_hbic",
-                 "fsqr_set_lambda_weights", "fsqr_lla"):
+                 "fsqr_set_lambda_weights", "fsqr_lla", "fsqr_pivotal"):
         getattr(L, name).restype = S
     _lib = L
     return L
@@ -313,6 +314,12 @@ def fsqr_lla(ctx, penalty: int, a: float, L: int, stream=None) -> dict:
                 objective=np.array([r.objective[i] for i in range(R)]))
 
 
+def fsqr_pivotal(ctx, rhs: int, B: int, seed: int = 0x5EED, stream=None) -> np.ndarray:
+    out = np.empty(int(B))
+    _check(load().fsqr_pivotal(ctx, int(rhs), int(B), ctypes.c_uint64(int(seed)), _ptr(out), _stream(stream)), ctx)
+    return out
+
+
 def fsqr_iterations(ctx) -> int:
     return int(load().fsqr_iterations(ctx))
 
@@ -416,6 +423,9 @@ class Solver:
 
     def lla(self, penalty: int, a: float, L: int = 1):
         return fsqr_lla(self.ctx, penalty, a, L)
+
+    def pivotal(self, B: int, seed: int = 0x5EED, rhs: int = 0):
+        return fsqr_pivotal(self.ctx, rhs, B, seed)
 
     def trace(self, rows: int = 4096):
         return fsqr_trace(self.ctx, self.R, rows)

@@ -38,6 +38,11 @@ void launch_build_support(const Dev& D, int par, cudaStream_t st);
 void launch_commit_stats(const Dev& D, double* pen, double* beta_out, int orig, cudaStream_t st);
 void launch_unfreeze(const Dev& D, cudaStream_t st);
 void launch_lla_weights(const Dev& D, int kind, double a, cudaStream_t st);
+cudaError_t pivotal_init();
+void launch_piv_draws(int n, int ldk, double tau, uint64_t seed, long long b0, int8_t* draws, int* nb,
+                      cudaStream_t st);
+void launch_pivotal(const Dev& D, const void* tmA, const void* tmX256, const int* nb, unsigned long long* lmax,
+                    int grid, cudaStream_t st);
 void launch_k1_mode(const Dev& D, int grid, cudaStream_t st, int cur);
 
 namespace {
@@ -73,6 +78,11 @@ struct fsqr_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool owns_stats = true;
   int64_t path_cap = 0;
+  // pivotal statistic (lazily allocated)
+  int8_t* piv_draws = nullptr;
+  int* piv_nb = nullptr;
+  unsigned long long* piv_lmax = nullptr;
+  CUtensorMap tmPivA{}, tmPivX{};
 };
 
 namespace {
@@ -780,6 +790,61 @@ fsqr_status fsqr_lla(fsqr_ctx* ctx, int32_t penalty, double a, int32_t L, int64_
   }
   if (out) *out = res;
   return last;
+}
+
+fsqr_status fsqr_pivotal(fsqr_ctx* ctx, int32_t rhs, int64_t B, uint64_t seed, double* Lambda_host, void* stream) {
+  if (!ctx || !Lambda_host) return set_err(ctx, FSQR_ERR_CONFIG, "null argument");
+  if (rhs < 0 || rhs >= ctx->R) return set_err(ctx, FSQR_ERR_CONFIG, "rhs %d out of range", rhs);
+  if (B < 1) return set_err(ctx, FSQR_ERR_CONFIG, "B must be >= 1");
+  if (ctx->D.storage != FSQR_U8) return set_err(ctx, FSQR_ERR_CONFIG, "the pivotal statistic needs U8 storage");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int ldk = (int)(((ctx->n + 127) / 128) * 128);
+  if (!ctx->piv_draws) {
+    AL(ctx->piv_draws, (size_t)128 * ldk);
+    AL(ctx->piv_nb, 128);
+    AL(ctx->piv_lmax, 128);
+    CK(pivotal_init());
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return set_err(ctx, FSQR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    EncodeTiledFn enc = (EncodeTiledFn)fn;
+    cuuint32_t es[2] = {1, 1};
+    {
+      cuuint64_t dims[2] = {(cuuint64_t)ldk, 128};
+      cuuint64_t strides[1] = {(cuuint64_t)ldk};
+      cuuint32_t box[2] = {128, 128};
+      CUresult r = enc(&ctx->tmPivA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)ctx->piv_draws, dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return set_err(ctx, FSQR_ERR_CUDA, "tensor map for the draws failed (%d)", (int)r);
+    }
+    {
+      cuuint64_t dims[2] = {(cuuint64_t)ctx->n, (cuuint64_t)ctx->p};
+      cuuint64_t strides[1] = {(cuuint64_t)ctx->D.ld};
+      cuuint32_t box[2] = {128, 256};
+      CUresult r = enc(&ctx->tmPivX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)ctx->D.X8, dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return set_err(ctx, FSQR_ERR_CUDA, "tensor map for X (256 rows) failed (%d)", (int)r);
+    }
+  }
+  const int grid = (int)std::min<int64_t>((ctx->p + 255) / 256, ctx->sms);
+  std::vector<unsigned long long> h(128);
+  for (int64_t b0 = 0; b0 < B; b0 += 128) {
+    launch_piv_draws((int)ctx->n, ldk, ctx->tau[rhs], seed, (long long)b0, ctx->piv_draws, ctx->piv_nb, st);
+    CK(cudaMemsetAsync(ctx->piv_lmax, 0, sizeof(unsigned long long) * 128, st));
+    launch_pivotal(ctx->D, &ctx->tmPivA, &ctx->tmPivX, ctx->piv_nb, ctx->piv_lmax, grid, st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h.data(), ctx->piv_lmax, sizeof(unsigned long long) * 128, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int64_t q = 0; q < 128 && b0 + q < B; ++q) {
+      double v;
+      memcpy(&v, &h[q], sizeof v);
+      Lambda_host[b0 + q] = v;
+    }
+  }
+  return FSQR_OK;
 }
 
 fsqr_status fsqr_kkt(fsqr_ctx* ctx, double* R_host, void* stream) {

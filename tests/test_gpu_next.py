@@ -100,3 +100,19 @@ def test_lla_bad_arguments(cuda_ok):
     bad[0, 3] = -1.0
     with pytest.raises(fs.FsqrError):
         S.set_lambda_weights(bad)
+
+
+@pytest.mark.parametrize("n,p,B,tau", [(1000, 3000, 300, 0.3), (777, 513, 129, 0.9)])
+def test_pivotal_statistic_matches_oracle(cuda_ok, n, p, B, tau):
+    """Lambda_b (L412, reading R18) on the tensor cores vs the oracle: ragged n (K tail), ragged p
+    (N tail of the 256-column tiles) and a partial last pass of 128 replicates."""
+    import paper_2601_02826_b200 as fs
+
+    prob = datagen.make("c5", n=n, p=p)
+    d = oracle.Design.from_problem(prob)
+    X, y = to_device(prob)
+    S = fs.Solver(X, prob.storage, prob.n, prob.p, prob.ld, y, [tau], [0.1], G=5, eta=[1.0] * 5)
+    L = S.pivotal(B, seed=1234)
+    Lo = oracle.pivotal(d, tau, B, seed=1234)
+    np.testing.assert_allclose(L, Lo, rtol=1e-10)
+    assert oracle.pivotal_lambda(L) == pytest.approx(oracle.pivotal_lambda(Lo), rel=1e-10)

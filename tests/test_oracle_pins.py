@@ -409,3 +409,47 @@ def test_lla_stages_are_weighted_l1_optima(kind, a, seed):
         prev = st["beta"]
     # the concave penalty lightens the shrinkage of large coefficients: stage weights <= 1
     assert np.all(out["stages"][1]["weights"] <= 1.0)
+
+
+# ----------------------------------------------------------------- pivotal statistic (L412, reading R18)
+
+def test_splitmix_reference_outputs():
+    g = GOLD["splitmix64"]
+    for st, ex in zip(g["state"], g["expect"]):
+        st = int(st, 16) if isinstance(st, str) else st
+        assert oracle.splitmix(st) == int(ex, 16)
+
+
+def test_pivotal_draws_are_bernoulli_tau():
+    for tau in (0.1, 0.5, 0.9):
+        u = np.array([[oracle.piv_uniform(77, b, i) for i in range(500)] for b in range(40)])
+        assert np.all((u >= 0) & (u < 1))
+        f = np.mean(u <= tau)
+        assert abs(f - tau) < 4 * np.sqrt(tau * (1 - tau) / u.size)
+
+
+def test_pivotal_second_moment_single_column():
+    """p = 1: (n Lambda_b)^2 = (x~^T psi_b)^2 with E psi = 0, Var psi = tau(1-tau), sum x~^2 = n-1,
+    so its mean over replicates is tau(1-tau)(n-1) (law of large numbers, ~2% sd at B = 4000)."""
+    prob = datagen.make("c2", n=300, p=1, seed=51)
+    d = oracle.Design.from_problem(prob)
+    tau = 0.3
+    L = oracle.pivotal(d, tau, 4000, seed=9)
+    m2 = np.mean((prob.n * L) ** 2)
+    assert m2 == pytest.approx(tau * (1 - tau) * (prob.n - 1), rel=0.1)
+
+
+def test_pivotal_invariances():
+    """Recoding every genotype as 2 - x flips the sign of x~ (|.| unchanged); permuting the
+    columns leaves the maximum unchanged."""
+    prob = datagen.make("c2", n=200, p=30, seed=52)
+    d = oracle.Design.from_problem(prob)
+    L = oracle.pivotal(d, 0.6, 50, seed=3)
+    Xr = prob.X.copy()
+    Xr[:, :prob.n] = 2 - Xr[:, :prob.n]
+    dr = oracle.Design(prob.storage, prob.n, prob.p, prob.ld, Xr)
+    np.testing.assert_allclose(oracle.pivotal(dr, 0.6, 50, seed=3), L, rtol=1e-12)
+    perm = np.random.default_rng(0).permutation(prob.p)
+    dp = oracle.Design(prob.storage, prob.n, prob.p, prob.ld, np.ascontiguousarray(prob.X[perm]))
+    np.testing.assert_array_equal(oracle.pivotal(dp, 0.6, 50, seed=3), L)
+    assert oracle.pivotal_lambda(L, 0.1, 1.1) == pytest.approx(1.1 * np.sort(L)[44])

@@ -98,6 +98,16 @@ def run(name, args):
                    k2_frac_of_peak=xbytes / (st[0] / args.steps / 1e3) / 1e9 / peak(),
                    support=int(S.trace(1)[-1, :, 4].max()))
         emit(rec, args.out)
+        if args.pivotal and prob.storage == datagen.STORAGE_U8 and len(tg) == 1:
+            S.pivotal(128, seed=1)          # first call allocates and builds its tensor maps
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            L = S.pivotal(args.pivotal, seed=7)
+            dt = time.perf_counter() - t0
+            s_ = np.sort(L)
+            emit(dict(base, taus=tg, mode="pivotal", B=args.pivotal, seconds=dt,
+                      passes=(args.pivotal + 127) // 128, x_gbs_per_pass=xbytes * ((args.pivotal + 127) // 128) / dt / 1e9,
+                      lambda_piv=float(1.1 * s_[int(np.ceil(0.9 * len(s_))) - 1]), lambda_max=float(lm[0])), args.out)
         if args.no_kkt:
             continue
         # time to KKT tolerance from the cold start
@@ -122,6 +132,7 @@ def main():
     ap.add_argument("--max-iter", dest="max_iter", type=int, default=20000)
     ap.add_argument("--backend", type=int, default=0)
     ap.add_argument("--no-kkt", action="store_true")
+    ap.add_argument("--pivotal", type=int, default=0, help="also time B pivotal replicates (u8, one RHS)")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     for name in args.configs.split(","):
