@@ -34,6 +34,11 @@ void launch_power_reduce(const Dev& D, const int64_t* bstart, const double* v, c
 void launch_power_norm(const Dev& D, double* v, const double* w, const double* nrm, const int* frozen,
                        cudaStream_t st);
 void launch_null_score(const double* y, int n, const double* tau, int R, double* psi, cudaStream_t st);
+void launch_power_fwd_int(const Dev& D, const int64_t* bstart, const double* v, const int* frozen, double* part,
+                          int S, double* u, double* Ug, cudaStream_t st);
+void launch_sum_parts(const double* part, int S, int G, int n, double* u, double* Ug, cudaStream_t st);
+void launch_back_int(const Dev& D, const double* u, const double* Ug, int per_block, const int* frozen, double* w,
+                     unsigned long long* maxbits, cudaStream_t st);
 void launch_build_support(const Dev& D, int par, cudaStream_t st);
 void launch_commit_stats(const Dev& D, double* pen, double* beta_out, int orig, cudaStream_t st);
 void launch_unfreeze(const Dev& D, cudaStream_t st);
@@ -250,6 +255,13 @@ fsqr_status power_method(fsqr_ctx* ctx, cudaStream_t st) {
   AL(u, (size_t)G * D.n);
   AL(est, G);
   AL(nrm, G);
+  const bool geno = D.storage != 0;
+  constexpr int S = 8;   // column slices per block in the genotype forward (partials summed in fixed order)
+  double *part = nullptr, *Ug = nullptr;
+  if (geno) {
+    AL(part, (size_t)S * G * D.n);
+    AL(Ug, G);
+  }
   CK(cudaMemcpyAsync(d_bs, bs.data(), sizeof(int64_t) * (G + 1), cudaMemcpyHostToDevice, st));
   launch_power_start(p1, ctx->opt.seed, v, st);
   launch_power_reduce(D, d_bs, v, v, d_frozen, est, nrm, st);
@@ -259,8 +271,13 @@ fsqr_status power_method(fsqr_ctx* ctx, cudaStream_t st) {
   std::vector<int> frozen(G, 0);
   int live = G;
   for (int it = 1; it <= ctx->opt.power_max_iter && live > 0; ++it) {
-    launch_power_fwd(D, d_bs, v, d_frozen, u, st);
-    launch_back_f64(D, u, 1, d_frozen, w, nullptr, st);
+    if (geno) {
+      launch_power_fwd_int(D, d_bs, v, d_frozen, part, S, u, Ug, st);
+      launch_back_int(D, u, Ug, 1, d_frozen, w, nullptr, st);
+    } else {
+      launch_power_fwd(D, d_bs, v, d_frozen, u, st);
+      launch_back_f64(D, u, 1, d_frozen, w, nullptr, st);
+    }
     launch_power_reduce(D, d_bs, v, w, d_frozen, est, nrm, st);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h_est.data(), est, sizeof(double) * G, cudaMemcpyDeviceToHost, st));
@@ -291,7 +308,17 @@ fsqr_status lambda_max(fsqr_ctx* ctx, cudaStream_t st) {
   AL(psi, (size_t)ctx->R * D.n);
   AL(mb, ctx->R);
   launch_null_score(D.y, D.n, D.tau, ctx->R, psi, st);
-  for (int r = 0; r < ctx->R; ++r) launch_back_f64(D, psi + (size_t)r * D.n, 0, nullptr, nullptr, mb + r, st);
+  if (D.storage != 0) {
+    double *tmp, *Us;
+    AL(tmp, D.n);
+    AL(Us, ctx->R);
+    for (int r = 0; r < ctx->R; ++r) {
+      launch_sum_parts(psi + (size_t)r * D.n, 1, 1, D.n, tmp, Us + r, st);
+      launch_back_int(D, psi + (size_t)r * D.n, Us + r, 0, nullptr, nullptr, mb + r, st);
+    }
+  } else {
+    for (int r = 0; r < ctx->R; ++r) launch_back_f64(D, psi + (size_t)r * D.n, 0, nullptr, nullptr, mb + r, st);
+  }
   CK(cudaGetLastError());
   std::vector<unsigned long long> h(ctx->R);
   CK(cudaMemcpyAsync(h.data(), mb, sizeof(unsigned long long) * ctx->R, cudaMemcpyDeviceToHost, st));

@@ -489,6 +489,109 @@ __global__ void k_back_f64(const Dev D, const double* u, int per_block, const in
   }
 }
 
+// ---- genotype-storage power / lambda_max products (a0', R3-R4): 16 rows per thread, vector loads
+
+// codes of rows i0..i0+15 of data column c (u8: one 16-byte load; 2-bit: one 4-byte load)
+template <int ST>
+__device__ __forceinline__ void codes16(const Dev& D, int64_t c, int i0, double (&x)[16]) {
+  if (ST == 1) {
+    const uint4 v = __ldcs((const uint4*)(D.X8 + c * D.ld + i0));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 16; ++q) x[q] = (double)((w[q >> 2] >> (8 * (q & 3))) & 0xFFu);
+  } else {
+    const uint32_t w = __ldcs((const uint32_t*)(D.X8 + c * D.ld + (i0 >> 2)));
+#pragma unroll
+    for (int q = 0; q < 16; ++q) x[q] = (double)((w >> (2 * q)) & 3u);
+  }
+}
+
+// part[s][g][i] = sum over the s-th of S contiguous slices of block g of x~_ij v_j
+//              = sum_j x_ij (v_j/s_j) - sum_j m_j v_j / s_j   (+ v_0 for the intercept)
+template <int ST>
+__global__ void __launch_bounds__(128) k_power_fwd_int(const Dev D, const int64_t* bstart, const double* v,
+                                                       const int* frozen, double* part, int S) {
+  const int g = blockIdx.y, s = blockIdx.z;
+  if (frozen[g]) return;
+  const int i0 = (blockIdx.x * blockDim.x + threadIdx.x) * 16;
+  if (i0 >= D.n) return;
+  const int64_t j0 = bstart[g], len = bstart[g + 1] - j0;
+  const int64_t a0 = j0 + len * s / S, a1 = j0 + len * (s + 1) / S;
+  double acc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+  double cterm = 0.0;
+  for (int64_t j = a0; j < a1; ++j) {
+    const double vj = v[j];
+    if (j == 0) {
+      cterm -= vj;
+      continue;
+    }
+    const int64_t c = j - 1;
+    const double a = D.inv_sd[c] * vj;
+    cterm = fma(D.mean[c], a, cterm);
+    double x[16];
+    codes16<ST>(D, c, i0, x);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc[q] = fma(x[q], a, acc[q]);
+  }
+  double* out = part + ((int64_t)s * D.G + g) * D.n;
+#pragma unroll
+  for (int q = 0; q < 16; ++q)
+    if (i0 + q < D.n) out[i0 + q] = acc[q] - cterm;
+}
+
+// u[g][i] = sum_s part[s][g][i] (fixed order); Ug[g] = sum_i u[g][i] (fixed block tree)
+__global__ void __launch_bounds__(1024) k_sum_parts(const double* part, int S, int G, int n, const int* frozen,
+                                                    double* u, double* Ug) {
+  __shared__ double smd[33];
+  const int g = blockIdx.x;
+  if (frozen && frozen[g]) return;
+  double t = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double a = 0.0;
+    for (int ss = 0; ss < S; ++ss) a += part[((int64_t)ss * G + g) * n + i];
+    u[(int64_t)g * n + i] = a;
+    t += a;
+  }
+  double tt[1] = {t};
+  block_sum<1>(tt, smd);
+  if (threadIdx.x == 0) Ug[g] = tt[0];
+}
+
+// w_j = sum_i x~_ij u_{g(j),i} = (sum_i x_ij u_i - m_j Ug) / s_j; lane = model column, 16 rows per step
+template <int ST>
+__global__ void __launch_bounds__(256) k_back_int(const Dev D, const double* u, const double* Ug, int per_block,
+                                                  const int* frozen, double* w, unsigned long long* maxbits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t jb = gw * 32; jb <= D.p; jb += nw * 32) {
+    const int64_t j = jb + lane;
+    const bool in = j <= D.p;
+    const int g = (per_block && in) ? block_of_col(D, j) : 0;
+    const bool live = in && !(frozen && frozen[g]);
+    const double* ug = u + (int64_t)g * D.n;
+    double acc = 0.0;
+    const int64_t c = j >= 1 ? j - 1 : 0;
+    if (live && j >= 1) {
+      for (int i0 = 0; i0 < D.n; i0 += 16) {
+        double x[16];
+        codes16<ST>(D, c, i0, x);
+        const int lim = min(16, D.n - i0);
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (q < lim) acc = fma(x[q], __ldg(ug + i0 + q), acc);
+      }
+    }
+    if (live) {
+      const double wj = (j == 0) ? Ug[g] : (acc - D.mean[c] * Ug[g]) * D.inv_sd[c];
+      if (w) w[j] = wj;
+      if (maxbits && j >= 1) atomicMax(maxbits, (unsigned long long)__double_as_longlong(fabs(wj)));
+    }
+  }
+}
+
 // per block g: est = v_g . w_g, nrm = ||w_g||  (one CTA per block, fixed order)
 __global__ void k_power_reduce(const int64_t* bstart, const double* v, const double* w, const int* frozen,
                                double* est, double* nrm) {
@@ -709,6 +812,21 @@ void launch_power_reduce(const Dev& D, const int64_t* bstart, const double* v, c
 void launch_power_norm(const Dev& D, double* v, const double* w, const double* nrm, const int* frozen,
                        cudaStream_t st) {
   k_power_norm<<<512, 256, 0, st>>>(D, v, w, nrm, frozen);
+}
+void launch_power_fwd_int(const Dev& D, const int64_t* bstart, const double* v, const int* frozen, double* part,
+                          int S, double* u, double* Ug, cudaStream_t st) {
+  dim3 grid((D.n + 2047) / 2048, D.G, S);
+  if (D.storage == 1) k_power_fwd_int<1><<<grid, 128, 0, st>>>(D, bstart, v, frozen, part, S);
+  else k_power_fwd_int<2><<<grid, 128, 0, st>>>(D, bstart, v, frozen, part, S);
+  k_sum_parts<<<D.G, 1024, 0, st>>>(part, S, D.G, D.n, frozen, u, Ug);
+}
+void launch_sum_parts(const double* part, int S, int G, int n, double* u, double* Ug, cudaStream_t st) {
+  k_sum_parts<<<G, 1024, 0, st>>>(part, S, G, n, nullptr, u, Ug);
+}
+void launch_back_int(const Dev& D, const double* u, const double* Ug, int per_block, const int* frozen, double* w,
+                     unsigned long long* maxbits, cudaStream_t st) {
+  if (D.storage == 1) k_back_int<1><<<148 * 8, 256, 0, st>>>(D, u, Ug, per_block, frozen, w, maxbits);
+  else k_back_int<2><<<148 * 8, 256, 0, st>>>(D, u, Ug, per_block, frozen, w, maxbits);
 }
 void launch_null_score(const double* y, int n, const double* tau, int R, double* psi, cudaStream_t st) {
   k_null_score<<<1, 1024, 0, st>>>(y, n, tau, R, psi);
