@@ -148,6 +148,12 @@ fsqr_status fsqr_kkt(fsqr_ctx* ctx, double* R_host, void* stream);
  * Uses the cached s = X~beta (no pass over X).  Blocking. */
 fsqr_status fsqr_hbic(fsqr_ctx* ctx, double* hbic_host, void* stream);
 
+/* Elastic-net quadratic weight per RHS (Remark 3; App. B missing, DESIGN.md
+ * reading R19): the objective gains (lambda2_r / 2) sum_{j>=1} beta_j^2 and the block prox becomes
+ *     beta+ = [(eta beta + g - lam)_+ - (-eta beta - g - lam)_+] / (eta + lambda2)   (E14 at 0).
+ * lam2_host [n_rhs], >= 0 and finite (else FSQR_ERR_CONFIG); 0 (the default) is the LASSO. */
+fsqr_status fsqr_set_lambda2(fsqr_ctx* ctx, const double* lam2_host);
+
 /* Per-RHS penalty weights (weighted l1, E4 L150-155): w_host [n_rhs][p+1], lam_jr = lambda_r * w_jr,
  * w >= 0 and finite (else FSQR_ERR_CONFIG), w_0 ignored; NULL restores unit weights.  The state is
  * kept (warm start).  Blocking. */

@@ -17,6 +17,8 @@ Parity status per function (DESIGN.md §4 repeats this table):
   lambda_max      pinned: textbook null model (beta=0, intercept = sample quantile) just above it
   solve           pinned: LP vertex enumeration + HiGHS (tiny), Prop. 1 certificate, partition
                   invariance, fixed-point property, geometric decay (Corollary 1)
+  prox_en / solve(lam2 > 0)  pinned: 1-D brute force of the elastic-net prox; lam2 = 0 bitwise
+                  equals E14; converged objective equals an SLSQP solve of the QP form (tiny inputs)
   penalty_deriv   pinned: SPEC worked values (SCAD, MCP), continuity at the knots, the LASSO limit
   lla             pinned: each stage is a weighted-l1 PQR whose optimum matches the LP brute force
                   with the stage's weights; Prop. 1 certificate per stage
@@ -58,7 +60,7 @@ class _Design(ctypes.Structure):
 class _Opts(ctypes.Structure):
     _fields_ = [("tau", ctypes.c_double), ("mu", ctypes.c_double), ("G", ctypes.c_int32),
                 ("check", ctypes.c_int32), ("eta", ctypes.c_void_p), ("lam", ctypes.c_void_p),
-                ("max_iter", ctypes.c_int64), ("tol", ctypes.c_double)]
+                ("max_iter", ctypes.c_int64), ("tol", ctypes.c_double), ("lam2", ctypes.c_double)]
 
 
 def _load():
@@ -79,6 +81,10 @@ def _load():
         lib.orc_fwdprod_range.argtypes = [DP, P, I64, I64, P]
         lib.orc_prox_beta.restype = D
         lib.orc_prox_beta.argtypes = [D, D, D, D]
+        lib.orc_prox_en.restype = D
+        lib.orc_prox_en.argtypes = [D, D, D, D, D]
+        lib.orc_objective_en.restype = D
+        lib.orc_objective_en.argtypes = [DP, P, D, P, D, P]
         lib.orc_prox_z.restype = D
         lib.orc_prox_z.argtypes = [D, D, D, D, I64]
         lib.orc_dual.restype = D
@@ -191,6 +197,15 @@ def prox_beta(beta, g, lam, eta) -> float:
     return _load().orc_prox_beta(beta, g, lam, eta)
 
 
+def prox_en(beta, g, lam1, lam2, eta) -> float:
+    """Elastic-net block prox (Remark 3, L347-349; reading R19)."""
+    return _load().orc_prox_en(beta, g, lam1, lam2, eta)
+
+
+def objective_en(d: Design, y, tau, lam_vec, lam2: float, beta) -> float:
+    return _load().orc_objective_en(d.ref, _p(_f64(y)), tau, _p(_f64(lam_vec)), float(lam2), _p(_f64(beta)))
+
+
 def prox_z(z, theta, mu, tau, n) -> float:
     return _load().orc_prox_z(z, theta, mu, tau, n)
 
@@ -252,7 +267,7 @@ def objective(d: Design, y, tau, lam_vec, beta) -> float:
 
 
 def solve(d: Design, y, tau: float, lam_vec, eta_vec, mu: float, G: int, max_iter: int = 1000,
-          tol: float = 1e-6, check: bool = True, state=None, trace: bool = False) -> dict:
+          tol: float = 1e-6, check: bool = True, state=None, trace: bool = False, lam2: float = 0.0) -> dict:
     """Algorithm 1 from (beta, z, theta) = state or the cold start (0, y, 0)."""
     y = _f64(y)
     lam_vec, eta_vec = _f64(lam_vec), _f64(eta_vec)
@@ -260,7 +275,7 @@ def solve(d: Design, y, tau: float, lam_vec, eta_vec, mu: float, G: int, max_ite
         beta, z, theta = np.zeros(d.p + 1), y.copy(), np.zeros(d.n)
     else:
         beta, z, theta = (_f64(a).copy() for a in state)
-    o = _Opts(tau, mu, G, 1 if check else 0, _p(eta_vec), _p(lam_vec), int(max_iter), tol)
+    o = _Opts(tau, mu, G, 1 if check else 0, _p(eta_vec), _p(lam_vec), int(max_iter), tol, float(lam2))
     it = ctypes.c_int64(0)
     R = np.empty(3)
     obj = ctypes.c_double(0.0)

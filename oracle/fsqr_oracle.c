@@ -54,6 +54,7 @@ typedef struct {
   const double* lam;    /* [p+1], lam[0] = 0 (intercept unpenalised) */
   int64_t max_iter;
   double tol;
+  double lam2;          /* elastic-net quadratic weight (Remark 3, L347-349; reading R19); 0 = E14 */
 } orc_opts;
 
 /* ---------------------------------------------------------------- design */
@@ -156,6 +157,13 @@ double orc_prox_beta(double beta, double g, double lam, double eta) {
   return (pos(eta * beta + g - lam) - pos(-eta * beta - g - lam)) / eta;
 }
 
+/* Elastic-net block prox (Remark 3, L347-349; App. B missing, reading R19):
+ *   argmin_b lam1 |b| + (lam2/2) b^2 - g b + (eta/2)(b - beta)^2
+ *   = [(eta*beta + g - lam1)_+ - (-eta*beta - g - lam1)_+] / (eta + lam2)   (E14 when lam2 = 0) */
+double orc_prox_en(double beta, double g, double lam1, double lam2, double eta) {
+  return (pos(eta * beta + g - lam1) - pos(-eta * beta - g - lam1)) / (eta + lam2);
+}
+
 /* E15: z+ = (z + theta/mu - tau/(n mu))_+ - (-z - theta/mu - (1-tau)/(n mu))_+ */
 double orc_prox_z(double z, double theta, double mu, double tau, int64_t n) {
   return pos(z + theta / mu - tau / ((double)n * mu)) - pos(-z - theta / mu - (1.0 - tau) / ((double)n * mu));
@@ -182,8 +190,9 @@ double orc_rho(double u, double tau) { return (tau - (u < 0.0 ? 1.0 : 0.0)) * u;
 /* --------------------------------------------------------- diagnostics */
 
 /* relative KKT residuals R_p, R_beta, R_z at w = (beta, z, theta) given g = X~^T theta and s = X~ beta */
-static void kkt_parts(int64_t n, int64_t p1, const double* y, double tau, const double* lam, const double* beta,
-                      const double* z, const double* theta, const double* g, const double* s, double* R) {
+static void kkt_parts(int64_t n, int64_t p1, const double* y, double tau, const double* lam, double lam2,
+                      const double* beta, const double* z, const double* theta, const double* g, const double* s,
+                      double* R) {
   double rp = 0, yy = 0, rb = 0, bb = 0, gg = 0, rz = 0, zz = 0, tt = 0;
   for (int64_t i = 0; i < n; ++i) {
     double r = s[i] + z[i] - y[i];
@@ -196,7 +205,8 @@ static void kkt_parts(int64_t n, int64_t p1, const double* y, double tau, const 
     tt += nt * nt;
   }
   for (int64_t j = 0; j < p1; ++j) {
-    double d = beta[j] - soft(beta[j] + g[j], lam[j]);
+    /* g_j - lam2 beta_j in lam_j d|beta_j| (lam2 = 0: the LASSO condition; intercept lam2 = 0) */
+    double d = beta[j] - soft(beta[j] + (g[j] - (j > 0 ? lam2 : 0.0) * beta[j]), lam[j]);
     rb += d * d;
     bb += beta[j] * beta[j];
     gg += g[j] * g[j];
@@ -213,9 +223,22 @@ void orc_kkt_rel(const orc_design* X, const double* y, double tau, const double*
   double* s = (double*)malloc(sizeof(double) * n);
   orc_backprod(X, theta, g);
   orc_fwdprod(X, beta, s);
-  kkt_parts(n, p1, y, tau, lam, beta, z, theta, g, s, R);
+  kkt_parts(n, p1, y, tau, lam, 0.0, beta, z, theta, g, s, R);
   free(g);
   free(s);
+}
+
+/* elastic-net objective: E1 + (lam2/2) sum_{j>=1} beta_j^2 (Remark 3, reading R19) */
+double orc_objective_en(const orc_design* X, const double* y, double tau, const double* lam, double lam2,
+                        const double* beta) {
+  int64_t n = X->n, p1 = X->p + 1;
+  double* s = (double*)malloc(sizeof(double) * n);
+  orc_fwdprod(X, beta, s);
+  double loss = 0.0, pen = 0.0;
+  for (int64_t i = 0; i < n; ++i) loss += orc_rho(y[i] - s[i], tau);
+  for (int64_t j = 1; j < p1; ++j) pen += lam[j] * fabs(beta[j]) + 0.5 * lam2 * beta[j] * beta[j];
+  free(s);
+  return loss / (double)n + pen;
 }
 
 /* E1 objective: (1/n) sum rho_tau(y - X~ beta) + sum_{j>=1} lam_j |beta_j| */
@@ -384,11 +407,14 @@ int orc_solve(const orc_design* X, const double* y, const orc_opts* o, double* b
     if (!o->check && k == o->max_iter && k > 0 && !trace) { status = 2; break; }
     orc_backprod(X, theta, g);
     double Rk[3];
-    kkt_parts(n, p1, y, o->tau, o->lam, beta, z, theta, g, s, Rk);
+    kkt_parts(n, p1, y, o->tau, o->lam, o->lam2, beta, z, theta, g, s, Rk);
     double loss = 0.0, pen = 0.0;
     int64_t nnz = 0;
     for (int64_t i = 0; i < n; ++i) loss += orc_rho(y[i] - s[i], o->tau);
-    for (int64_t j = 1; j < p1; ++j) { pen += o->lam[j] * fabs(beta[j]); nnz += beta[j] != 0.0; }
+    for (int64_t j = 1; j < p1; ++j) {
+      pen += o->lam[j] * fabs(beta[j]) + 0.5 * o->lam2 * beta[j] * beta[j];
+      nnz += beta[j] != 0.0;
+    }
     double ob = loss / (double)n + pen;
     if (trace) {
       trace[5 * k + 0] = Rk[0];
@@ -404,7 +430,9 @@ int orc_solve(const orc_design* X, const double* y, const orc_opts* o, double* b
     if (o->check && Rmax <= o->tol) { status = 0; break; }
     if (k == o->max_iter) { status = 2; break; }
     /* ParFor g: beta_g^{k+1} by E14 */
-    for (int64_t j = 0; j < p1; ++j) beta[j] = orc_prox_beta(beta[j], g[j], o->lam[j], o->eta[blk[j]]);
+    for (int64_t j = 0; j < p1; ++j)
+      beta[j] = o->lam2 == 0.0 || j == 0 ? orc_prox_beta(beta[j], g[j], o->lam[j], o->eta[blk[j]])
+                                         : orc_prox_en(beta[j], g[j], o->lam[j], o->lam2, o->eta[blk[j]]);
     /* z^{k+1} by E15 (uses z^k, theta^k) */
     for (int64_t i = 0; i < n; ++i) z[i] = orc_prox_z(z[i], theta[i], o->mu, o->tau, n);
     /* theta^{k+1} by E12 */
@@ -456,7 +484,7 @@ int64_t orc_path(const orc_design* X, const double* y, double tau, double mu, in
   for (;; ++k) {
     orc_backprod(X, theta, g);
     double Rk[3];
-    kkt_parts(n, p1, y, tau, lam, beta, z, theta, g, s, Rk);
+    kkt_parts(n, p1, y, tau, lam, 0.0, beta, z, theta, g, s, Rk);
     double Rmax = fmax(Rk[0], fmax(Rk[1], Rk[2]));
     int switch_now = 0;
     if (Rmax <= tol || kpt == max_iter_point) {

@@ -56,7 +56,7 @@ class fsqr_result(ctypes.Structure):
 EXPORTS = ["fsqr_default_options", "fsqr_create", "fsqr_iterate", "fsqr_solve", "fsqr_objective", "fsqr_kkt",
            "fsqr_get_beta", "fsqr_get_state", "fsqr_set_state", "fsqr_set_lambda", "fsqr_lambda_max",
            "fsqr_get_eta", "fsqr_get_colstats", "fsqr_path", "fsqr_path_beta", "fsqr_trace", "fsqr_iterations",
-           "fsqr_profile_iterate", "fsqr_hbic", "fsqr_set_lambda_weights", "fsqr_lla", "fsqr_pivotal",
+           "fsqr_profile_iterate", "fsqr_hbic", "fsqr_set_lambda_weights", "fsqr_lla", "fsqr_pivotal", "fsqr_set_lambda2",
            "fsqr_backend_name", "fsqr_fit_host", "fsqr_last_error", "fsqr_global_error", "fsqr_status_str",
            "fsqr_destroy"]
 
@@ -102,6 +102,7 @@ def load(build_if_missing: bool = True):
     L.fsqr_profile_iterate.argtypes = [ctxp, I64, P, P, P]
     L.fsqr_profile_iterate.restype = S
     L.fsqr_hbic.argtypes = [ctxp, P, P]
+    L.fsqr_set_lambda2.argtypes = [ctxp, P]
     L.fsqr_pivotal.argtypes = [ctxp, I32, I64, ctypes.c_uint64, P, P]
     L.fsqr_set_lambda_weights.argtypes = [ctxp, P, P]
     L.fsqr_lla.argtypes = [ctxp, I32, D, I32, P, ctypes.POINTER(fsqr_result), P]
@@ -122,7 +123,7 @@ def load(build_if_missing: bool = True):
     for name in ("fsqr_create", "fsqr_iterate", "fsqr_solve", "fsqr_objective", "fsqr_kkt", "fsqr_get_beta",
                  "fsqr_get_state", "fsqr_set_state", "fsqr_set_lambda", "fsqr_lambda_max", "fsqr_get_eta",
                  "fsqr_get_colstats", "fsqr_path", "fsqr_path_beta", "fsqr_trace", "fsqr_fit_host", "fsqr_hbic",
-                 "fsqr_set_lambda_weights", "fsqr_lla", "fsqr_pivotal"):
+                 "fsqr_set_lambda_weights", "fsqr_lla", "fsqr_pivotal", "fsqr_set_lambda2"):
         getattr(L, name).restype = S
     _lib = L
     return L
@@ -298,6 +299,11 @@ def fsqr_hbic(ctx, n_rhs: int, stream=None) -> np.ndarray:
     return out
 
 
+def fsqr_set_lambda2(ctx, lam2):
+    v = np.ascontiguousarray(lam2, dtype=np.float64)
+    return _check(load().fsqr_set_lambda2(ctx, _ptr(v)), ctx)
+
+
 def fsqr_set_lambda_weights(ctx, weights=None, stream=None):
     """weights: [n_rhs, p+1] (or None for unit weights)."""
     w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
@@ -417,6 +423,9 @@ class Solver:
 
     def hbic(self):
         return fsqr_hbic(self.ctx, self.R)
+
+    def set_lambda2(self, lam2):
+        return fsqr_set_lambda2(self.ctx, lam2)
 
     def set_lambda_weights(self, weights=None):
         return fsqr_set_lambda_weights(self.ctx, weights)

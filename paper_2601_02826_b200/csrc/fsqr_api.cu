@@ -496,6 +496,7 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
   D.tau = tau_d;
   D.lam_cur = lam_cur;
   // penalty weights: ctx-owned [(p+1)][R]; the caller's [p+1] vector (if any) is broadcast to every RHS
+  AL(D.lam2, R);
   AL(D.lamw, p1 * R);
   AL(D.use_w, 1);
   if (lamw_dev) {
@@ -788,6 +789,15 @@ fsqr_status fsqr_set_lambda_weights(fsqr_ctx* ctx, const double* w_host, void* s
   }
   CK(cudaMemcpyAsync(ctx->D.use_w, &flag, sizeof(int), cudaMemcpyHostToDevice, st));
   CK(cudaStreamSynchronize(st));
+  return FSQR_OK;
+}
+
+fsqr_status fsqr_set_lambda2(fsqr_ctx* ctx, const double* lam2_host) {
+  if (!ctx || !lam2_host) return set_err(ctx, FSQR_ERR_CONFIG, "null argument");
+  for (int r = 0; r < ctx->R; ++r)
+    if (!(lam2_host[r] >= 0.0) || !std::isfinite(lam2_host[r]))
+      return set_err(ctx, FSQR_ERR_CONFIG, "lambda2[%d]=%g invalid", r, lam2_host[r]);
+  CK(cudaMemcpy(ctx->D.lam2, lam2_host, sizeof(double) * ctx->R, cudaMemcpyHostToDevice));
   return FSQR_OK;
 }
 

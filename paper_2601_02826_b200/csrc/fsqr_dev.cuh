@@ -73,6 +73,7 @@ struct Dev {
   // per-RHS control
   const double* tau;                // [R]
   double* lam_cur;                  // [R]
+  double* lam2;                     // [R] elastic-net quadratic weights (0 = LASSO / weighted l1)
   double* scal;                     // [R][FSQR_NSCAL]
   int* status;                      // [R]
   long long* commit_iter;           // [R]
@@ -297,6 +298,7 @@ struct K2Ctx {
   int R;
   bool active[RMAX];
   double lam[RMAX];
+  double lam2[RMAX];        // elastic-net quadratic weight (reading R19)
   double gscale[RMAX];      // delta_r / n (genotype storage)
   long long Tsum[RMAX];
 };
@@ -335,14 +337,17 @@ __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, i
     const double b = C.beta_in[j * C.R + r];
     const double lam = C.use_w ? C.lam[r] * D.lamw[j * C.R + r] : C.lam[r];
     // KKT residual part of w^k and penalty at beta^k
-    const double d = b - soft_thr(b + g[r], lam);
+    const double l2 = C.lam2[r];
+    const double d = b - soft_thr(b + (g[r] - l2 * b), lam);   // KKT: g - lam2 b in lam d|b|
     P.v[r][0] += d * d;
     P.v[r][1] += b * b;
     P.v[r][2] += g[r] * g[r];
-    P.v[r][3] += lam * fabs(b);
+    P.v[r][3] += lam * fabs(b) + 0.5 * l2 * b * b;
     P.v[r][4] += (b != 0.0) ? 1.0 : 0.0;
     if (D.update) {
-      const double bn = prox_beta(b, g[r], lam, eta);
+      // E14, or the elastic-net block prox (Remark 3, L347-349; reading R19) when lam2 > 0
+      const double bn = l2 == 0.0 ? prox_beta(b, g[r], lam, eta)
+                                  : (pos_part(eta * b + g[r] - lam) - pos_part(-eta * b - g[r] - lam)) / (eta + l2);
       C.beta_out[j * C.R + r] = bn;
       if (bn != 0.0) {
         nz = true;

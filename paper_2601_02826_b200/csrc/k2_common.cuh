@@ -21,6 +21,7 @@ __device__ void k2_load_ctx(const Dev& D, K2Ctx<RMAX>& C) {
     const bool a = r < D.R && D.status[r] == ST_ACTIVE;
     C.active[r] = a;
     C.lam[r] = r < D.R ? D.lam_cur[r] : 0.0;
+    C.lam2[r] = r < D.R ? D.lam2[r] : 0.0;
     C.gscale[r] = r < D.R ? D.delta[r] / (double)D.n : 0.0;
     C.Tsum[r] = r < D.R ? D.Tsum[r] : 0;
   }

@@ -712,7 +712,7 @@ __global__ void __launch_bounds__(FT) k_commit_stats(const Dev D, double* pen_ou
     for (int64_t j = 1 + threadIdx.x; j <= D.p; j += blockDim.x) {
       const double b = beta[j * D.R + r];
       const double lam = use_w ? D.lam_cur[r] * D.lamw[j * D.R + r] : D.lam_cur[r];
-      a[0] += lam * fabs(b);
+      a[0] += lam * fabs(b) + 0.5 * D.lam2[r] * b * b;
       const double bo = b * D.inv_sd[j - 1];
       a[1] += D.mean[j - 1] * bo;
       a[2] += b != 0.0 ? 1.0 : 0.0;

@@ -116,3 +116,26 @@ def test_pivotal_statistic_matches_oracle(cuda_ok, n, p, B, tau):
     Lo = oracle.pivotal(d, tau, B, seed=1234)
     np.testing.assert_allclose(L, Lo, rtol=1e-10)
     assert oracle.pivotal_lambda(L) == pytest.approx(oracle.pivotal_lambda(Lo), rel=1e-10)
+
+
+@pytest.mark.parametrize("storage,lam2", [(1, 0.5), (2, 2.0)])
+def test_elastic_net_matches_oracle(cuda_ok, storage, lam2):
+    """Weighted elastic net (Remark 3, reading R19): fixed iterations and convergence to KKT 1e-6."""
+    name = "c2" if storage == 1 else "c4"
+    prob, d, S, c = _setup(name=name, n=700, p=1600, storage=storage)
+    S.set_lambda2([lam2])
+    lv = oracle.lam_vector(prob.p, c["lam"])
+    S.iterate(120)
+    b, z, t = S.state()
+    o = oracle.solve(d, prob.y, c["tau"], lv, c["eta"], c["mu"], c["G"], max_iter=120, check=False, lam2=lam2)
+    assert rel(b[0], o["beta"]) < 1e-6
+    assert rel(t[0], o["theta"]) < 1e-6
+    assert np.array_equal(b[0] != 0, o["beta"] != 0)
+    res = S.solve()
+    assert res["status"] == 0
+    oc = oracle.solve(d, prob.y, c["tau"], lv, c["eta"], c["mu"], c["G"], max_iter=200000, tol=1e-6, lam2=lam2,
+                      state=(o["beta"], o["z"], o["theta"]))
+    assert oc["status"] == 0
+    bb = S.beta()[0]
+    assert rel(bb, oc["beta"]) < 1e-4
+    assert S.objective()[0] == pytest.approx(oracle.objective_en(d, prob.y, c["tau"], lv, lam2, oc["beta"]), rel=1e-4)

@@ -453,3 +453,50 @@ def test_pivotal_invariances():
     dp = oracle.Design(prob.storage, prob.n, prob.p, prob.ld, np.ascontiguousarray(prob.X[perm]))
     np.testing.assert_array_equal(oracle.pivotal(dp, 0.6, 50, seed=3), L)
     assert oracle.pivotal_lambda(L, 0.1, 1.1) == pytest.approx(1.1 * np.sort(L)[44])
+
+
+# ----------------------------------------------------------------- elastic net (Remark 3, reading R19)
+
+def test_prox_en_bruteforce_and_lasso_limit():
+    """argmin_b lam1|b| + (lam2/2) b^2 - g b + (eta/2)(b - beta)^2 (the weighted elastic-net block
+    prox); with lam2 = 0 it is E14 bit for bit."""
+    rng = np.random.default_rng(3)
+    for _ in range(60):
+        beta, g = rng.normal(), rng.normal()
+        lam1, lam2, eta = abs(rng.normal()) * rng.choice([0, 0.3, 1]), rng.uniform(0, 3), rng.uniform(0.2, 5)
+        f = lambda b: lam1 * abs(b) + 0.5 * lam2 * b * b - g * b + 0.5 * eta * (b - beta) ** 2
+        assert oracle.prox_en(beta, g, lam1, lam2, eta) == pytest.approx(_argmin_1d(f, -20, 20), abs=1e-7)
+        assert oracle.prox_en(beta, g, lam1, 0.0, eta) == oracle.prox_beta(beta, g, lam1, eta)
+
+
+@pytest.mark.parametrize("seed,tau,lam2", [(61, 0.5, 0.3), (62, 0.25, 1.0)])
+def test_elastic_net_solve_matches_qp(seed, tau, lam2):
+    """Algorithm 1 with the elastic-net prox converges to the optimum of
+    (1/n) sum rho_tau + sum lam_j |b_j| + (lam2/2) sum_{j>=1} b_j^2, solved independently as a
+    smooth QP (u, v, a, b >= 0 split) by SLSQP on a tiny instance."""
+    from scipy.optimize import minimize
+
+    prob, d = _tiny(seed, n=12, p=3)
+    A, _, _ = _np_standardized(prob)
+    lm, _ = oracle.lambda_max(d, prob.y, tau)
+    lam = oracle.lam_vector(prob.p, 0.2 * lm)
+    G, mu = 2, 0.1
+    eta = oracle.eta(d, G, mu)
+    out = oracle.solve(d, prob.y, tau, lam, eta, mu, G, max_iter=400000, tol=1e-11, lam2=lam2)
+    assert out["status"] == 0
+    n, p = prob.n, prob.p
+    # variables: beta0, a (p), b (p), u (n), v (n)
+    def f(x):
+        a, b, u, v = x[1:1 + p], x[1 + p:1 + 2 * p], x[1 + 2 * p:1 + 2 * p + n], x[1 + 2 * p + n:]
+        return (tau * u.sum() + (1 - tau) * v.sum()) / n + np.sum(lam[1:] * (a + b)) + 0.5 * lam2 * np.sum((a - b) ** 2)
+    def eq(x):
+        beta = np.concatenate([[x[0]], x[1:1 + p] - x[1 + p:1 + 2 * p]])
+        return prob.y - A @ beta - (x[1 + 2 * p:1 + 2 * p + n] - x[1 + 2 * p + n:])
+    x0 = np.zeros(1 + 2 * p + 2 * n)
+    x0[1 + 2 * p:1 + 2 * p + n] = np.maximum(prob.y, 0)
+    x0[1 + 2 * p + n:] = np.maximum(-prob.y, 0)
+    res = minimize(f, x0, method="SLSQP", constraints=[{"type": "eq", "fun": eq}],
+                   bounds=[(None, None)] + [(0, None)] * (2 * p + 2 * n), options=dict(ftol=1e-14, maxiter=2000))
+    assert res.success
+    assert out["obj"] == pytest.approx(res.fun, rel=1e-6, abs=1e-10)
+    assert oracle.objective_en(d, prob.y, tau, lam, lam2, out["beta"]) == pytest.approx(out["obj"], rel=1e-12)
