@@ -444,6 +444,10 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
   D.gq = (X->p + 1) / o.G;
   D.grem = (X->p + 1) % o.G;
   D.npad = ((4 * R + 15) / 16) * 16;
+  D.k1_policy = 0;
+  D.x_policy = 0;
+  if (const char* ev = getenv("FSQR_X_POLICY")) D.x_policy = atoi(ev);
+  if (const char* ev = getenv("FSQR_K1_POLICY")) D.k1_policy = atoi(ev);
   D.ldk = (int)(((X->n + 127) / 128) * 128);
   D.X8 = X->storage != 0 ? (const uint8_t*)X->data_dev : nullptr;
   D.Xf = X->storage == 0 ? (const float*)X->data_dev : nullptr;
@@ -535,7 +539,7 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
   AL(D.kbase, 1);
   AL(D.fpart, (size_t)FIN_MAXGRID * R * FSQR_FPART);
   AL(D.ftsum, (size_t)FIN_MAXGRID * R);
-  AL(D.fticket, 1);
+  AL(D.fticket, 1 + FSQR_MAXR);
   AL(D.scal, R * FSQR_NSCAL);
   AL(D.status, R);
   AL(D.commit_iter, R);

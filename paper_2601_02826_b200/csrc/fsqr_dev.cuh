@@ -31,6 +31,8 @@ enum { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_NUMERIC = 3 };
 struct Dev {
   // sizes / layout
   int n, R, G, storage, npad, ldk;
+  int x_policy;                     // L2 hint of the X stream in K2: 0 evict_first, 1 normal, 2 evict_last
+  int k1_policy;                    // L2 hint of the forward gather: 0 evict_first, 1 normal, 2 evict_last
   int bperm;                        // 1: theta digit rows in the 2-bit tcgen05 K order (k2_tc2.cu)
   int64_t p, ld;
   int64_t gq, grem;                 // block partition of the p+1 model columns: q = (p+1)/G, rem
@@ -69,7 +71,7 @@ struct Dev {
   // multi-CTA finalize partials + ticket
   double* fpart;                    // [FIN_MAXGRID][R][FSQR_FPART]
   long long* ftsum;                 // [FIN_MAXGRID][R]
-  unsigned int* fticket;
+  unsigned int* fticket;            // [1 + MAXR]: overall, then per RHS
   // per-RHS control
   const double* tau;                // [R]
   double* lam_cur;                  // [R]
@@ -218,6 +220,11 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, uint64_
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ uint64_t policy_evict_last() {

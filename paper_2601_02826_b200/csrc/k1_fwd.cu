@@ -80,6 +80,33 @@ __device__ __forceinline__ void seg_codes(const uint8_t* seg, int t, uint32_t (&
   }
 }
 
+// one support column of a stage: x * C_lo and x * C_hi into the int32 accumulators of the
+// thread's RPT rows (u8 codes zero-extended with one PRMT each)
+template <int RPT, int ST, int RMAX>
+__device__ __forceinline__ void consume_col(const uint8_t* seg, const int32_t* cf, int tid,
+                                            int32_t (&alo)[RPT][RMAX], int32_t (&ahi)[RPT][RMAX]) {
+  uint32_t x[RPT];
+  if (ST == 1 && RPT == 8) {
+    const uint2 v = *(const uint2*)(seg + 8 * tid);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      x[i] = __byte_perm(v.x, 0u, 0x4440u + i);
+      x[4 + i] = __byte_perm(v.y, 0u, 0x4440u + i);
+    }
+  } else {
+    seg_codes<RPT, ST>(seg, tid, x);
+  }
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) {
+    const int2 c = *(const int2*)(cf + 2 * r);
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      alo[i][r] += (int32_t)x[i] * c.x;
+      ahi[i][r] += (int32_t)x[i] * c.y;
+    }
+  }
+}
+
 template <int RMAX, int ST>
 struct K1Smem {
   static constexpr int RPT = K1Shape<RMAX>::RPT;
@@ -145,7 +172,8 @@ __global__ void __launch_bounds__(KTHREADS) k1_bulk(const Dev D, int cur) {
       const double cm = r < R ? __longlong_as_double((long long)D.cmax[par * R + r]) : 0.0;
       scale[r] = ldexp(1.0, fwd_exponent(cm, cnt, D.n));
     }
-    const uint64_t pol = policy_evict_first();
+    const uint64_t pol = D.k1_policy == 2 ? policy_evict_last()
+                         : (D.k1_policy == 1 ? policy_evict_normal() : policy_evict_first());
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
@@ -235,18 +263,11 @@ __global__ void __launch_bounds__(KTHREADS) k1_bulk(const Dev D, int cur) {
           const int nq = min(QC, ng - q0);
           const uint8_t* sd = sdata + stage * QC * SEG;
           const int32_t* cf = scoef + stage * QC * RMAX * 2;
-          for (int q = 0; q < nq; ++q) {
-            uint32_t x[RPT];
-            seg_codes<RPT, ST>(sd + q * SEG, tid, x);
+          if (nq == QC) {
 #pragma unroll
-            for (int r = 0; r < RMAX; ++r) {
-              const int32_t lo = cf[(q * RMAX + r) * 2], hi = cf[(q * RMAX + r) * 2 + 1];
-#pragma unroll
-              for (int i = 0; i < RPT; ++i) {
-                alo[i][r] += (int32_t)x[i] * lo;
-                ahi[i][r] += (int32_t)x[i] * hi;
-              }
-            }
+            for (int q = 0; q < QC; ++q) consume_col<RPT, ST, RMAX>(sd + q * SEG, cf + q * RMAX * 2, tid, alo, ahi);
+          } else {
+            for (int q = 0; q < nq; ++q) consume_col<RPT, ST, RMAX>(sd + q * SEG, cf + q * RMAX * 2, tid, alo, ahi);
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[stage]);

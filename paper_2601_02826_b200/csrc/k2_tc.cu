@@ -106,7 +106,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (wid == 0) {
     // ===== TMA producer: the whole warp walks the ring, one elected lane issues =====
     {
-      const uint64_t pol_x = policy_evict_first(), pol_b = policy_evict_last();
+      const uint64_t pol_x = D.x_policy == 2 ? policy_evict_last()
+                             : (D.x_policy == 1 ? policy_evict_normal() : policy_evict_first());
+      const uint64_t pol_b = policy_evict_last();
       const uint32_t bytes = (uint32_t)(A_BYTES + 4 * D.R * 128);
       int stage = 0;
       uint32_t phase = 0;

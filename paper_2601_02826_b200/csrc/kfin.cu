@@ -236,6 +236,8 @@ __device__ __forceinline__ int theta_exponent(double mx) {
 }
 
 __global__ void __launch_bounds__(FIN_THREADS) k_finalize_mc(const Dev D) {
+  // grid (ceil(n/256), R): CTA (x, r) owns rows 256x.. of RHS r.  Tickets: fticket[1 + r] elects the
+  // last CTA of RHS r (its fixed-order reduction), fticket[0] the last CTA overall (iteration tail).
   __shared__ double smd[32 * 8 + 8];
   __shared__ long long smll[33];
   __shared__ bool s_last;
@@ -243,9 +245,10 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize_mc(const Dev D) {
   const long long k = *D.iter;
   const int par = (int)(k & 1), par1 = par ^ 1;
   const int n = D.n;
+  const int r = blockIdx.y;
   const int i = blockIdx.x * FIN_THREADS + threadIdx.x;
-  for (int r = 0; r < D.R; ++r) {
-    if (D.status[r] != ST_ACTIVE) continue;
+  const int nblk = gridDim.x;
+  if (D.status[r] == ST_ACTIVE) {
     const double b0 = D.beta[par][r] + D.sumth[r] / D.eta[0];   // E14 with lambda_0 = 0, g_0 = sum theta^k
     const double tau = D.tau[r];
     const double mu = D.mu, sig = D.sigma;
@@ -284,67 +287,69 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize_mc(const Dev D) {
       ts = quant_row(D, r, i, thn, inv_prev);
     }
     block_sum<7>(*(double(*)[7])acc, smd);
-    const double mx = block_max(acc[7], smd);
+    const double mxb = block_max(acc[7], smd);
     ts = block_sum_ll(ts, smll);
     if (threadIdx.x == 0) {
       double* fp = D.fpart + ((size_t)blockIdx.x * D.R + r) * FSQR_FPART;
       for (int q = 0; q < 7; ++q) fp[q] = acc[q];
-      fp[7] = mx;
+      fp[7] = mxb;
       D.ftsum[(size_t)blockIdx.x * D.R + r] = ts;
     }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(D.fticket + 1 + r, 1u) == (unsigned)nblk - 1;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      // ---------------------------------------- last CTA of RHS r: fixed-order reduction over its CTAs
+      __shared__ double s_dlt;
+      __shared__ int s_requant;
+      double a[7];
+      reduce_records<7>(D.fpart + (size_t)r * FSQR_FPART, nblk, D.R * FSQR_FPART, a, smd);
+      double mxl = 0.0;
+      long long tsl = 0;
+      for (int b = threadIdx.x; b < nblk; b += FIN_THREADS) {
+        const double m = D.fpart[((size_t)b * D.R + r) * FSQR_FPART + 7];
+        mxl = (m > mxl || !isfinite(m)) ? m : mxl;
+        tsl += D.ftsum[(size_t)b * D.R + r];
+      }
+      const double mx = block_max(mxl, smd);
+      const long long tsum = block_sum_ll(tsl, smll);
+      if (threadIdx.x == 0) {
+        double* sc = D.scal + r * FSQR_NSCAL;
+        sc[0] = sqrt(a[0]) / (1.0 + sqrt(a[6]));
+        sc[1] = sqrt(a[3]) / (1.0 + sqrt(a[1]) + sqrt(a[2]));
+        sc[2] = a[4];
+        sc[3] = a[6];
+        D.beta[par1][r] = b0;
+        D.sumth[r] = a[5];
+        D.mterm[r] = 0;
+        const int e_new = theta_exponent(mx);
+        const int e_old = theta_exponent(D.delta[r] * ldexp(1.0, 28) * 0.75);   // delta^k = 2^(e_old - 28)
+        s_requant = (e_new != e_old) ? 1 : 0;
+        const double dlt = (mx > 0.0 && isfinite(mx)) ? ldexp(1.0, e_new - 28) : 1.0;
+        s_dlt = dlt;
+        if (!s_requant) D.Tsum[r] = tsum;
+        D.delta[r] = dlt;
+        D.fticket[1 + r] = 0u;
+      }
+      __syncthreads();
+      if (s_requant) {
+        const double inv = 1.0 / s_dlt;
+        long long t2 = 0;
+        for (int ii = threadIdx.x; ii < n; ii += FIN_THREADS) t2 += quant_row(D, r, ii, D.theta[(int64_t)r * n + ii], inv);
+        t2 = block_sum_ll(t2, smll);
+        if (threadIdx.x == 0) D.Tsum[r] = t2;
+      }
+    }
   }
+  // ------------------------------------------------ last CTA overall: iteration tail
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(D.fticket, 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) s_last = atomicAdd(D.fticket, 1u) == (unsigned)(nblk * D.R) - 1;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // ------------------------------------------------ last CTA: fixed-order reduction over CTAs
-  for (int r = 0; r < D.R; ++r) {
-    if (D.status[r] != ST_ACTIVE) continue;
-    __shared__ double s_mx;
-    __shared__ int s_requant;
-    double a[7];
-    reduce_records<7>(D.fpart + (size_t)r * FSQR_FPART, (int)gridDim.x, D.R * FSQR_FPART, a, smd);
-    double mxl = 0.0;
-    long long tsl = 0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += FIN_THREADS) {
-      const double m = D.fpart[((size_t)b * D.R + r) * FSQR_FPART + 7];
-      mxl = (m > mxl || !isfinite(m)) ? m : mxl;
-      tsl += D.ftsum[(size_t)b * D.R + r];
-    }
-    const double mx = block_max(mxl, smd);
-    const long long ts = block_sum_ll(tsl, smll);
-    if (threadIdx.x == 0) {
-      double* sc = D.scal + r * FSQR_NSCAL;
-      sc[0] = sqrt(a[0]) / (1.0 + sqrt(a[6]));
-      sc[1] = sqrt(a[3]) / (1.0 + sqrt(a[1]) + sqrt(a[2]));
-      sc[2] = a[4];
-      sc[3] = a[6];
-      const double b0 = D.beta[par][r] + D.sumth[r] / D.eta[0];
-      D.beta[par1][r] = b0;
-      D.sumth[r] = a[5];
-      D.mterm[r] = 0;
-      const int e_new = theta_exponent(mx);
-      const int e_old = theta_exponent(D.delta[r] * ldexp(1.0, 28) * 0.75);   // delta^k = 2^(e_old - 28)
-      s_requant = (e_new != e_old) ? 1 : 0;
-      const double dlt = (mx > 0.0 && isfinite(mx)) ? ldexp(1.0, e_new - 28) : 1.0;
-      s_mx = dlt;
-      if (!s_requant) {
-        D.Tsum[r] = ts;
-      }
-      D.delta[r] = dlt;
-    }
-    __syncthreads();
-    if (s_requant) {
-      const double inv = 1.0 / s_mx;
-      long long ts = 0;
-      for (int ii = threadIdx.x; ii < n; ii += FIN_THREADS) ts += quant_row(D, r, ii, D.theta[(int64_t)r * n + ii], inv);
-      ts = block_sum_ll(ts, smll);
-      if (threadIdx.x == 0) D.Tsum[r] = ts;
-    }
-    __syncthreads();
-  }
   if (threadIdx.x < D.R) D.cmax[par * D.R + threadIdx.x] = 0ull;
   if (threadIdx.x == 0) {
     D.sup_cnt[par] = 0;
@@ -783,7 +788,7 @@ void launch_finalize(const Dev& D, cudaStream_t st) {
   if (D.storage == 0)
     k_finalize<<<1, FT, 0, st>>>(D);
   else
-    k_finalize_mc<<<(D.n + FIN_THREADS - 1) / FIN_THREADS, FIN_THREADS, 0, st>>>(D);
+    k_finalize_mc<<<dim3((D.n + FIN_THREADS - 1) / FIN_THREADS, D.R), FIN_THREADS, 0, st>>>(D);
 }
 void launch_init_state(const Dev& D, cudaStream_t st) { k_init_state<<<1, FT, 0, st>>>(D); }
 void launch_colstats(const Dev& D, int32_t* colsum, double* mean, double* inv_sd, double* sd, int* bad,
