@@ -50,6 +50,8 @@ void launch_pivotal(const Dev& D, const void* tmA, const void* tmX256, const int
                     int grid, cudaStream_t st);
 void launch_k1_mode(const Dev& D, int grid, cudaStream_t st, int cur);
 
+int g_fsqr_pdl = 1;   // FSQR_PDL=0 launches the hot path without programmatic dependent launch
+
 namespace {
 
 thread_local std::string g_err;
@@ -444,6 +446,7 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
   D.gq = (X->p + 1) / o.G;
   D.grem = (X->p + 1) % o.G;
   D.npad = ((4 * R + 15) / 16) * 16;
+  if (const char* ev = getenv("FSQR_PDL")) g_fsqr_pdl = atoi(ev) != 0;
   D.k1_policy = 0;
   D.x_policy = 0;
   if (const char* ev = getenv("FSQR_X_POLICY")) D.x_policy = atoi(ev);

@@ -236,6 +236,12 @@ __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
 
+// Programmatic dependent launch: every hot-path kernel lets the next one be scheduled at once
+// (its prologue -- barrier init, TMEM allocation, tensor-map prefetch -- overlaps this kernel's
+// tail) and waits for the previous grid's completion (memory visible) before touching state.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // one lane of a converged warp (the tcgen05.mma issuer); operands computed before the branch stay
 // warp-uniform, so ptxas keeps them in uniform registers (no per-MMA waterfall)
 __device__ __forceinline__ bool elect_one() {
@@ -263,6 +269,11 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
 }
 
 // instruction descriptor: kind::i8, D = s32, A = s8, B = s8, both K-major, M = 128, N = npad
+// same with an UNSIGNED 8-bit A operand (k2_tc2's plane-split codes reach 2 * 64 = 128)
+__host__ __device__ constexpr uint32_t idesc_u8s8(int N) {
+  return (2u << 4) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
 __host__ __device__ constexpr uint32_t idesc_i8(int N) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
@@ -400,6 +411,24 @@ __device__ __forceinline__ double g_from_digits(int n, int32_t colsum, long long
 }
 
 // ------------------------------------------------------------------ host launchers (one per TU)
+
+extern int g_fsqr_pdl;   // 1: hot-path kernels are launched with programmatic stream serialization
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_fsqr_pdl;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 struct LaunchCfg {
   int grid;

@@ -134,6 +134,8 @@ __global__ void __launch_bounds__(KTHREADS) k1_bulk(const Dev D, int cur) {
   uint64_t* full = (uint64_t*)(sm + SH::DATA + SH::COEF);
   uint64_t* empty = full + STAGES;
 
+  pdl_launch_dependents();
+  pdl_wait();
   if (*D.stop) return;
   const long long k = *D.iter;
   const int par = (int)((k + (cur ? 0 : 1)) & 1);
@@ -304,6 +306,8 @@ __global__ void __launch_bounds__(KTHREADS) k1_bulk(const Dev D, int cur) {
 // fp32 design: s_i = sum_j (x_ij - m_j) beta_j / s_j in ascending j (beta_0 added by finalize)
 template <int RMAX>
 __global__ void __launch_bounds__(THREADS) k1_f32(const Dev D, int cur) {
+  pdl_launch_dependents();
+  pdl_wait();
   if (*D.stop) return;
   const long long k = *D.iter;
   const double* beta = D.beta[(int)((k + (cur ? 0 : 1)) & 1)];
@@ -341,11 +345,11 @@ int bulk_grid(int grid) {
 template <int RMAX>
 void launch_r(const Dev& D, int grid, cudaStream_t st, int cur) {
   if (D.storage == 0)
-    k1_f32<RMAX><<<(D.n + THREADS - 1) / THREADS, THREADS, 0, st>>>(D, cur);
+    launch_pdl(k1_f32<RMAX>, dim3((D.n + THREADS - 1) / THREADS), dim3(THREADS), 0, st, D, cur);
   else if (D.storage == 1)
-    k1_bulk<RMAX, 1><<<bulk_grid<RMAX, 1>(grid), KTHREADS, K1Smem<RMAX, 1>::BYTES, st>>>(D, cur);
+    launch_pdl(k1_bulk<RMAX, 1>, dim3(bulk_grid<RMAX, 1>(grid)), dim3(KTHREADS), K1Smem<RMAX, 1>::BYTES, st, D, cur);
   else
-    k1_bulk<RMAX, 2><<<bulk_grid<RMAX, 2>(grid), KTHREADS, K1Smem<RMAX, 2>::BYTES, st>>>(D, cur);
+    launch_pdl(k1_bulk<RMAX, 2>, dim3(bulk_grid<RMAX, 2>(grid)), dim3(KTHREADS), K1Smem<RMAX, 2>::BYTES, st, D, cur);
 }
 
 template <int RMAX>

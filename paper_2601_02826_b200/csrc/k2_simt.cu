@@ -26,6 +26,8 @@ __global__ void __launch_bounds__(THREADS) k2_simt_int(const Dev D) {
   constexpr int CPW = RMAX <= 2 ? 4 : (RMAX <= 4 ? 2 : 1);   // columns per warp
   constexpr int ND = 4 * RMAX;                                 // digit rows
   __shared__ double red[K2_RED_DOUBLES(RMAX)];
+  pdl_launch_dependents();
+  pdl_wait();
   if (*D.stop) return;
   K2Ctx<RMAX> C;
   k2_load_ctx(D, C);
@@ -113,6 +115,8 @@ __global__ void __launch_bounds__(THREADS) k2_simt_int(const Dev D) {
 template <int RMAX>
 __global__ void __launch_bounds__(THREADS) k2_simt_f32(const Dev D) {
   __shared__ double red[K2_RED_DOUBLES(RMAX)];
+  pdl_launch_dependents();
+  pdl_wait();
   if (*D.stop) return;
   K2Ctx<RMAX> C;
   k2_load_ctx(D, C);
@@ -151,11 +155,11 @@ __global__ void __launch_bounds__(THREADS) k2_simt_f32(const Dev D) {
 template <int RMAX>
 void launch_r(const Dev& D, int grid, cudaStream_t st) {
   if (D.storage == 0)
-    k2_simt_f32<RMAX><<<grid, THREADS, 0, st>>>(D);
+    launch_pdl(k2_simt_f32<RMAX>, dim3(grid), dim3(THREADS), 0, st, D);
   else if (D.storage == 1)
-    k2_simt_int<RMAX, 1><<<grid, THREADS, 0, st>>>(D);
+    launch_pdl(k2_simt_int<RMAX, 1>, dim3(grid), dim3(THREADS), 0, st, D);
   else
-    k2_simt_int<RMAX, 2><<<grid, THREADS, 0, st>>>(D);
+    launch_pdl(k2_simt_int<RMAX, 2>, dim3(grid), dim3(THREADS), 0, st, D);
 }
 
 }  // namespace

@@ -45,7 +45,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     k2_tc_kernel(const Dev D, const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmB) {
   using CF = Cfg<NPAD, RM>;
   constexpr int RMAX = CF::RMAX;
-  if (*D.stop) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
@@ -60,11 +59,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   const int64_t ntiles = (D.p + TILE_M - 1) / TILE_M;
   const int kblocks = (D.n + TILE_K - 1) / TILE_K;
-
-  K2Ctx<RMAX> C;
-  k2_load_ctx(D, C);
-  K2Part<RMAX> P;
-  P.zero();
 
   if (wid == 0 && lane == 0) {
     prefetch_tmap(&tmX);
@@ -102,6 +96,22 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_launch_dependents();
+  pdl_wait();
+  if (*D.stop) {   // uniform: every thread reads the same flag
+    tc_fence_before();
+    __syncthreads();
+    if (wid == 2) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(CF::TMEM_COLS)
+                   : "memory");
+    }
+    return;
+  }
+  K2Ctx<RMAX> C;
+  k2_load_ctx(D, C);
+  K2Part<RMAX> P;
+  P.zero();
 
   if (wid == 0) {
     // ===== TMA producer: the whole warp walks the ring, one elected lane issues =====
@@ -216,7 +226,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 template <int NPAD, int RM>
 void launch_np(const Dev& D, const void* tmX, const void* tmB, int grid, cudaStream_t st) {
-  k2_tc_kernel<NPAD, RM><<<grid, THREADS, Cfg<NPAD, RM>::SMEM, st>>>(D, *(const CUtensorMap*)tmX,
+  launch_pdl(k2_tc_kernel<NPAD, RM>, dim3(grid), dim3(THREADS), Cfg<NPAD, RM>::SMEM, st, D, *(const CUtensorMap*)tmX,
                                                                 *(const CUtensorMap*)tmB);
 }
 

@@ -43,6 +43,11 @@ constexpr int A_COL0 = 128;               // A buffers start after the accumulat
 template <int NPAD, int RM>
 struct Cfg2 {
   static constexpr int CW = RM == 1 ? 8 : 4;
+  // NPAD == 16: one accumulator per code plane q, so the converter can leave the codes in place
+  // ((w & (3 << 2q)) = x * 4^q, one LOP per word instead of shift + mask); the epilogue divides
+  // each plane's exact sum by 4^q.  Needs 2 x 4 x 16 = 128 TMEM columns (fits before A_COL0).
+  static constexpr bool SPLITQ = NPAD == 16;
+  static constexpr int ACC_COLS = SPLITQ ? 4 * NPAD : NPAD;   // columns of one accumulator buffer
   static constexpr int THREADS = 32 * (8 + CW);
   static constexpr int B_ATOM = NPAD * 128;
   static constexpr int B_BYTES = 4 * B_ATOM;
@@ -92,7 +97,6 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
   constexpr int CW = CF::CW;
   constexpr int THREADS = CF::THREADS;
   constexpr int EPI0 = 4 + CW;   // first epilogue warp
-  if (*D.stop) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
@@ -109,11 +113,6 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   const int64_t ntiles = (D.p + TILE_M - 1) / TILE_M;
   const int kblocks = (int)((D.ld + PK - 1) / PK);
-
-  K2Ctx<RMAX> C;
-  k2_load_ctx(D, C);
-  K2Part<RMAX> P;
-  P.zero();
 
   if (wid == 0 && lane == 0) {
     prefetch_tmap(&tmX);
@@ -155,6 +154,21 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_launch_dependents();
+  pdl_wait();
+  if (*D.stop) {   // uniform: every thread reads the same flag
+    tc_fence_before();
+    __syncthreads();
+    if (wid == 2) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
+    }
+    return;
+  }
+  K2Ctx<RMAX> C;
+  k2_load_ctx(D, C);
+  K2Part<RMAX> P;
+  P.zero();
 
   if (wid == 0) {
     // ===== TMA producer: the whole warp walks the ring, one elected lane issues =====
@@ -186,7 +200,7 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
   } else if (wid == 1) {
     // ===== MMA issuer: the whole warp walks the pipeline, one elected lane issues =====
     {
-      constexpr uint32_t idesc = idesc_i8(NPAD);
+      constexpr uint32_t idesc = CF::SPLITQ ? idesc_u8s8(NPAD) : idesc_i8(NPAD);
       const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
       const uint32_t sB0 = smem_u32(sB);
       int stage = 0, ab = 0;
@@ -197,7 +211,7 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
         const uint32_t tph = (lt >> 1) & 1;
         mbar_wait(&tempty[acc], tph ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tbase + (uint32_t)(acc * NPAD);
+        const uint32_t d_tmem = tbase + (uint32_t)(acc * CF::ACC_COLS);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&full[stage], phase);
           mbar_wait(&afull[ab], aphase);
@@ -206,9 +220,12 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
           const uint64_t bdesc0 = umma_desc_sw128(sB0 + (uint32_t)(stage * CF::B_BYTES));
           if (elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < KS / 32; ++kk)   // K = 32 samples per kind::i8 MMA
-              umma_i8_tmem_a(d_tmem, a_tmem + (uint32_t)(8 * kk),
-                             bdesc0 + (uint64_t)((kk >> 2) * (CF::B_ATOM >> 4) + 2 * (kk & 3)), idesc, (kb | kk) != 0);
+            for (int kk = 0; kk < KS / 32; ++kk) {   // K = 32 samples per kind::i8 MMA; plane q = kk / 4
+              const uint32_t dq = CF::SPLITQ ? d_tmem + (uint32_t)((kk >> 2) * NPAD) : d_tmem;
+              const bool accum = CF::SPLITQ ? (kb != 0 || (kk & 3) != 0) : (kb | kk) != 0;
+              umma_i8_tmem_a(dq, a_tmem + (uint32_t)(8 * kk),
+                             bdesc0 + (uint64_t)((kk >> 2) * (CF::B_ATOM >> 4) + 2 * (kk & 3)), idesc, accum);
+            }
             umma_commit(&empty[stage]);
             umma_commit(&aempty[ab]);
           }
@@ -258,7 +275,8 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
         for (int q = 0; q < 4; ++q) {
           uint32_t o[NW];
 #pragma unroll
-          for (int u = 0; u < NW; ++u) o[u] = (w[u] >> (2 * q)) & 0x03030303u;
+          for (int u = 0; u < NW; ++u)
+            o[u] = CF::SPLITQ ? (w[u] & (0x03030303u << (2 * q))) : ((w[u] >> (2 * q)) & 0x03030303u);
           if constexpr (NW == 32) tmem_st32(abase + (uint32_t)(32 * q), o);
           else tmem_st16(abase + (uint32_t)(32 * q), o);
         }
@@ -286,13 +304,26 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       int32_t dv[NPAD];
+      if constexpr (CF::SPLITQ) {
 #pragma unroll
-      for (int h = 0; h < NPAD / 16; ++h) {
-        uint32_t v[16];
-        tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NPAD + h * 16), v);
-        tmem_wait_ld();
+        for (int u = 0; u < NPAD; ++u) dv[u] = 0;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) dv[h * 16 + u] = (int32_t)v[u];
+        for (int pq = 0; pq < 4; ++pq) {   // plane pq holds 4^pq x its exact sum: divide exactly
+          uint32_t v[16];
+          tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * CF::ACC_COLS + pq * NPAD), v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int u = 0; u < 16; ++u) dv[u] += ((int32_t)v[u]) >> (2 * pq);
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < NPAD / 16; ++h) {
+          uint32_t v[16];
+          tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NPAD + h * 16), v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int u = 0; u < 16; ++u) dv[h * 16 + u] = (int32_t)v[u];
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -327,7 +358,8 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
 
 template <int NPAD, int RM>
 void launch_np(const Dev& D, const void* tmX, const void* tmB, int grid, cudaStream_t st) {
-  k2_tc2_kernel<NPAD, RM><<<grid, Cfg2<NPAD, RM>::THREADS, Cfg2<NPAD, RM>::SMEM, st>>>(D, *(const CUtensorMap*)tmX,
+  launch_pdl(k2_tc2_kernel<NPAD, RM>, dim3(grid), dim3(Cfg2<NPAD, RM>::THREADS), Cfg2<NPAD, RM>::SMEM, st, D,
+             *(const CUtensorMap*)tmX,
                                                                 *(const CUtensorMap*)tmB);
 }
 

@@ -185,6 +185,8 @@ __device__ void nvec_step(const Dev& D, int r, int mode, double b0, int fwd_par,
 __global__ void __launch_bounds__(FT) k_finalize(const Dev D) {
   __shared__ double smd[32 * 8 + 8];
   __shared__ long long smll[33];
+  pdl_launch_dependents();
+  pdl_wait();
   if (*D.stop) return;
   const long long k = *D.iter;
   const int par = (int)(k & 1), par1 = par ^ 1;
@@ -241,6 +243,8 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize_mc(const Dev D) {
   __shared__ double smd[32 * 8 + 8];
   __shared__ long long smll[33];
   __shared__ bool s_last;
+  pdl_launch_dependents();
+  pdl_wait();
   if (*D.stop) return;
   const long long k = *D.iter;
   const int par = (int)(k & 1), par1 = par ^ 1;
@@ -786,9 +790,9 @@ __global__ void k_unfreeze(const Dev D) {
 
 void launch_finalize(const Dev& D, cudaStream_t st) {
   if (D.storage == 0)
-    k_finalize<<<1, FT, 0, st>>>(D);
+    launch_pdl(k_finalize, dim3(1), dim3(FT), 0, st, D);
   else
-    k_finalize_mc<<<dim3((D.n + FIN_THREADS - 1) / FIN_THREADS, D.R), FIN_THREADS, 0, st>>>(D);
+    launch_pdl(k_finalize_mc, dim3((D.n + FIN_THREADS - 1) / FIN_THREADS, D.R), dim3(FIN_THREADS), 0, st, D);
 }
 void launch_init_state(const Dev& D, cudaStream_t st) { k_init_state<<<1, FT, 0, st>>>(D); }
 void launch_colstats(const Dev& D, int32_t* colsum, double* mean, double* inv_sd, double* sd, int* bad,

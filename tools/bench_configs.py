@@ -91,8 +91,17 @@ def run(name, args):
         lam = [prob.lam_frac * v for v in lm]
         S.set_lambda(lam)
         S.iterate(args.burn_in)
+        # graph-chunk iterations (the solver's own launch path), device time with CUDA events
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        kg = max(args.steps, 4 * 16)
+        e0.record()
+        S.iterate(kg)
+        e1.record()
+        torch.cuda.synchronize()
+        graph_ips = kg / (e0.elapsed_time(e1) / 1e3)
         st, tot = fs.fsqr_profile_iterate(S.ctx, args.steps)
         rec.update(mode="iters", lam=lam, burn_in=args.burn_in, steps=args.steps, ms_per_step=tot / args.steps,
+                   graph_iters_per_s=graph_ips,
                    iters_per_s=args.steps / (tot / 1e3), stage_ms=(st / args.steps).tolist(),
                    x_gbs=xbytes / (tot / args.steps / 1e3) / 1e9,
                    k2_frac_of_peak=xbytes / (st[0] / args.steps / 1e3) / 1e9 / peak(),
