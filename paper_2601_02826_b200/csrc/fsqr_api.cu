@@ -73,7 +73,7 @@ struct fsqr_ctx {
   int sms = 148;
   int k2_grid = 148, k1_grid = 148;
   int chunk = 16;
-  CUtensorMap tmX{}, tmB{};
+  CUtensorMap tmX{}, tmB{}, tmG{};
   cudaStream_t cap_stream = nullptr;
   std::vector<void*> allocs;
   std::string err;
@@ -168,6 +168,18 @@ fsqr_status make_tmaps(fsqr_ctx* ctx) {
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_err(ctx, FSQR_ERR_CUDA, "tensor map for theta digits failed (%d)", (int)r);
+  }
+  if (D.k1_tc == 2) {
+    // forward gather: 128-row windows of single columns, four columns per tile::gather4
+    cuuint64_t dims[2] = {(cuuint64_t)D.ld, (cuuint64_t)D.p};
+    cuuint64_t strides[1] = {(cuuint64_t)D.ld};
+    cuuint32_t box[2] = {128, 1};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(&ctx->tmG, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)D.X8, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(ctx, FSQR_ERR_CUDA, "tensor map for the forward gather failed (%d)", (int)r);
+    ctx->D.tmG = &ctx->tmG;
   }
   return FSQR_OK;
 }
@@ -481,8 +493,21 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
   } else {
     ctx->k2_grid = ctx->sms * 8;
   }
-  ctx->k1_grid = ctx->sms;   // k1_bulk scales by its resident CTAs per SM
+  ctx->k1_grid = ctx->sms;   // k1_bulk scales by its resident CTAs per SM; k1_tc runs one CTA per SM
   CK(k1_init());
+  // forward-product kernel: with 3+ RHS the CUDA-core kernel's 2R multiply-adds per element lose
+  // to the gather4 tensor-core kernel (C5 at 0.05 lambda_max: 0.80 vs 2.43 ms); with 1-2 RHS the
+  // gather's one TMA operation per 512 bytes is the slower side (M: 140 vs 55 us).
+  // FSQR_K1=bulk|tc|gather overrides, for measurements.
+  D.k1_tc = 0;
+  if (ctx->backend == FSQR_BACKEND_TC && X->storage == FSQR_U8 && R >= 3) D.k1_tc = 2;
+  if (const char* ev = getenv("FSQR_K1")) {
+    if (!strcmp(ev, "bulk")) D.k1_tc = 0;
+    else if (!strcmp(ev, "tc") && X->storage != FSQR_F32_DENSE) D.k1_tc = 1;
+    else if (!strcmp(ev, "gather") && X->storage == FSQR_U8) D.k1_tc = 2;
+  }
+  if (D.k1_tc == 1) CK(k1_tc_init());
+  if (D.k1_tc == 2) CK(k1_tcg_init());
 
   // ---------------- allocations
   int32_t* colsum;

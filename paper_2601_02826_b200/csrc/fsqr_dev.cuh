@@ -31,6 +31,8 @@ enum { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_NUMERIC = 3 };
 struct Dev {
   // sizes / layout
   int n, R, G, storage, npad, ldk;
+  int k1_tc;                        // forward product: 0 k1_bulk (CUDA cores), 1 k1_tc (TMEM transpose), 2 k1_tcg (gather4)
+  const void* tmG;                  // host pointer to the gather4 tensor map (launcher side only)
   int x_policy;                     // L2 hint of the X stream in K2: 0 evict_first, 1 normal, 2 evict_last
   int k1_policy;                    // L2 hint of the forward gather: 0 evict_first, 1 normal, 2 evict_last
   int bperm;                        // 1: theta digit rows in the 2-bit tcgen05 K order (k2_tc2.cu)
@@ -303,6 +305,17 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 
 // ------------------------------------------------------------------ per-launch K2 context
 
+// per-RHS constants of one K2 launch, in shared memory (read once per column; keeping them in
+// registers costs ~9 registers per RHS and spilled the 9-RHS epilogue)
+template <int RMAX>
+struct K2Const {
+  double lam[RMAX];
+  double lam2[RMAX];        // elastic-net quadratic weight (reading R19)
+  double gscale[RMAX];      // delta_r / n (genotype storage)
+  long long Tsum[RMAX];
+  int active[RMAX];
+};
+
 template <int RMAX>
 struct K2Ctx {
   long long k;
@@ -314,11 +327,7 @@ struct K2Ctx {
   double* sb;
   int* scnt;
   int R;
-  bool active[RMAX];
-  double lam[RMAX];
-  double lam2[RMAX];        // elastic-net quadratic weight (reading R19)
-  double gscale[RMAX];      // delta_r / n (genotype storage)
-  long long Tsum[RMAX];
+  const K2Const<RMAX>* cs;  // shared memory
 };
 
 // per-thread fp64 partials
@@ -351,11 +360,11 @@ __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, i
   for (int r = 0; r < RMAX; ++r) {
     cval[r] = 0.0;
     bval[r] = 0.0;
-    if (r >= C.R || !C.active[r]) continue;
+    if (r >= C.R || !C.cs->active[r]) continue;
     const double b = C.beta_in[j * C.R + r];
-    const double lam = C.use_w ? C.lam[r] * D.lamw[j * C.R + r] : C.lam[r];
+    const double lam = C.use_w ? C.cs->lam[r] * D.lamw[j * C.R + r] : C.cs->lam[r];
     // KKT residual part of w^k and penalty at beta^k
-    const double l2 = C.lam2[r];
+    const double l2 = C.cs->lam2[r];
     const double d = b - soft_thr(b + (g[r] - l2 * b), lam);   // KKT: g - lam2 b in lam d|b|
     P.v[r][0] += d * d;
     P.v[r][1] += b * b;
@@ -444,4 +453,8 @@ void launch_finalize(const Dev& D, cudaStream_t st);
 int k2_tc_smem_bytes(int npad);
 cudaError_t k2_tc_init();
 cudaError_t k1_init();
+cudaError_t k1_tc_init();
+cudaError_t k1_tcg_init();
+void launch_k1_tcg(const Dev& D, const void* tmG, int grid, cudaStream_t st, int cur);
+void launch_k1_tc(const Dev& D, int grid, cudaStream_t st, int cur);
 int k2_tc_supported(int npad);

@@ -16,15 +16,17 @@ __device__ void k2_load_ctx(const Dev& D, K2Ctx<RMAX>& C) {
   C.sb = D.sup_b[par ^ 1];
   C.scnt = D.sup_cnt + (par ^ 1);
   C.R = D.R;
-#pragma unroll
-  for (int r = 0; r < RMAX; ++r) {
-    const bool a = r < D.R && D.status[r] == ST_ACTIVE;
-    C.active[r] = a;
-    C.lam[r] = r < D.R ? D.lam_cur[r] : 0.0;
-    C.lam2[r] = r < D.R ? D.lam2[r] : 0.0;
-    C.gscale[r] = r < D.R ? D.delta[r] / (double)D.n : 0.0;
-    C.Tsum[r] = r < D.R ? D.Tsum[r] : 0;
+  __shared__ K2Const<RMAX> k2c;   // every thread of the block calls this (then a block barrier)
+  if (threadIdx.x < RMAX) {
+    const int r = threadIdx.x;
+    k2c.active[r] = r < D.R && D.status[r] == ST_ACTIVE;
+    k2c.lam[r] = r < D.R ? D.lam_cur[r] : 0.0;
+    k2c.lam2[r] = r < D.R ? D.lam2[r] : 0.0;
+    k2c.gscale[r] = r < D.R ? D.delta[r] / (double)D.n : 0.0;
+    k2c.Tsum[r] = r < D.R ? D.Tsum[r] : 0;
   }
+  __syncthreads();
+  C.cs = &k2c;
 }
 
 // Block reduction of the per-thread partials (fixed order), publication of the
@@ -84,7 +86,7 @@ __device__ void k2_finish(const Dev& D, const K2Ctx<RMAX>& C, K2Part<RMAX>& P, d
   if (tid < C.R) {
     const int r = tid;
     s_rec[r] = -1;
-    if (C.active[r]) {
+    if (C.cs->active[r]) {
       double a[FSQR_NPART];
       for (int q = 0; q < FSQR_NPART; ++q) a[q] = s_tot[r][q];
       const double g0 = D.sumth[r], b0 = C.beta_in[r];

@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(THREADS) k2_simt_int(const Dev D) {
         const double isd = D.inv_sd[c];
 #pragma unroll
         for (int r = 0; r < RMAX; ++r)
-          g[r] = r < C.R ? g_from_digits(D.n, cs, C.Tsum[r], C.gscale[r], isd, &acc[a][4 * r]) : 0.0;
+          g[r] = r < C.R ? g_from_digits(D.n, cs, C.cs->Tsum[r], C.cs->gscale[r], isd, &acc[a][4 * r]) : 0.0;
         nz = epi_column<RMAX>(D, C, c, g, P, cval, bval);
       }
     }

@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const double isd = D.inv_sd[c];
 #pragma unroll
         for (int r = 0; r < RMAX; ++r)
-          g[r] = r < C.R ? g_from_digits(D.n, cs, C.Tsum[r], C.gscale[r], isd, dv + 4 * r) : 0.0;
+          g[r] = r < C.R ? g_from_digits(D.n, cs, C.cs->Tsum[r], C.cs->gscale[r], isd, dv + 4 * r) : 0.0;
         nz = epi_column<RMAX>(D, C, c, g, P, cval, bval);
       } else {
 #pragma unroll
