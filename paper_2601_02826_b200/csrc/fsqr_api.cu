@@ -505,6 +505,7 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
     if (!strcmp(ev, "bulk")) D.k1_tc = 0;
     else if (!strcmp(ev, "tc") && X->storage != FSQR_F32_DENSE) D.k1_tc = 1;
     else if (!strcmp(ev, "gather") && X->storage == FSQR_U8) D.k1_tc = 2;
+
   }
   if (D.k1_tc == 1) CK(k1_tc_init());
   if (D.k1_tc == 2) CK(k1_tcg_init());

@@ -33,7 +33,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // rows per thread: keep 4 * RPT * RMAX int32-equivalent accumulator registers <= 64
-template <int RMAX>
+// (measured at M: 16 rows per thread / 4 KB copies was slower (58 vs 53 us); an fp64
+// one-DFMA-per-element variant ran the same 53 us as the two-IMAD one)
+template <int RMAX, int ST>
 struct K1Shape {
   static constexpr int RPT = RMAX <= 2 ? 8 : (RMAX <= 4 ? 4 : (RMAX <= 8 ? 2 : 1));
   static constexpr int RPW = 256 * RPT;
@@ -43,7 +45,12 @@ struct K1Shape {
 template <int RPT, int ST>
 __device__ __forceinline__ void seg_codes(const uint8_t* seg, int t, uint32_t (&x)[RPT]) {
   if (ST == 1) {
-    if (RPT == 8) {
+    if (RPT == 16) {
+      const uint4 v = *(const uint4*)(seg + 16 * t);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 16; ++q) x[q] = __byte_perm(w[q >> 2], 0u, 0x4440u + (q & 3));
+    } else if (RPT == 8) {
       const uint2 v = *(const uint2*)(seg + 8 * t);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -63,7 +70,18 @@ __device__ __forceinline__ void seg_codes(const uint8_t* seg, int t, uint32_t (&
     }
   } else {
     // 2-bit: row i at bits 2(i%4) of byte i/4
-    if (RPT == 8) {
+    if (RPT == 32) {
+      const uint2 v = *(const uint2*)(seg + 8 * t);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        x[q] = (v.x >> (2 * q)) & 3u;
+        x[16 + q] = (v.y >> (2 * q)) & 3u;
+      }
+    } else if (RPT == 16) {
+      const uint32_t v = *(const uint32_t*)(seg + 4 * t);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) x[q] = (v >> (2 * q)) & 3u;
+    } else if (RPT == 8) {
       const uint32_t v = *(const uint16_t*)(seg + 2 * t);
 #pragma unroll
       for (int q = 0; q < 8; ++q) x[q] = (v >> (2 * q)) & 3u;
@@ -109,7 +127,7 @@ __device__ __forceinline__ void consume_col(const uint8_t* seg, const int32_t* c
 
 template <int RMAX, int ST>
 struct K1Smem {
-  static constexpr int RPT = K1Shape<RMAX>::RPT;
+  static constexpr int RPT = K1Shape<RMAX, ST>::RPT;
   static constexpr int SEG = ST == 1 ? 256 * RPT : 64 * RPT;   // bytes of one column's slab segment
   static constexpr int QC = SEG >= 2048 ? 8 : (SEG >= 1024 ? 16 : 32);   // columns per stage (divides 32)
   static constexpr int ST0 = (96 * 1024) / (QC * SEG);
@@ -128,7 +146,7 @@ __global__ void __launch_bounds__(KTHREADS) k1_bulk(const Dev D, int cur) {
   constexpr int RPW = 256 * RPT;
   constexpr int SEG = SH::SEG;
   extern __shared__ uint8_t k1_smem_raw[];
-  uint8_t* sm = (uint8_t*)(((uintptr_t)k1_smem_raw + 127) & ~(uintptr_t)127);
+  uint8_t* sm = k1_smem_raw + (((127 + 1) - (smem_u32(k1_smem_raw) & 127)) & 127);
   uint8_t* sdata = sm;
   int32_t* scoef = (int32_t*)(sm + SH::DATA);
   uint64_t* full = (uint64_t*)(sm + SH::DATA + SH::COEF);
@@ -186,21 +204,44 @@ __global__ void __launch_bounds__(KTHREADS) k1_bulk(const Dev D, int cur) {
       long long mt[RMAX];
 #pragma unroll
       for (int r = 0; r < RMAX; ++r) mt[r] = 0;
+      // software pipeline: the next group's (column, beta/s) loads are in flight while this group's
+      // stages are issued, and its colsum load after them
+      int32_t ncol = 0;
+      double nsc[RMAX];
+      long long ncs = 0;
+      {
+        const int64_t e = e0 + lane;
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r) nsc[r] = 0.0;
+        if (e < e1) {
+          ncol = sidx[e];
+#pragma unroll
+          for (int r = 0; r < RMAX; ++r) nsc[r] = r < R ? sc[e * R + r] : 0.0;
+          ncs = (slab == 0) ? (long long)D.colsum[ncol] : 0;
+        }
+      }
       for (int64_t g0 = e0; g0 < e1; g0 += 32) {
         const int64_t e = g0 + lane;
-        int32_t col = 0;
+        const int32_t col = ncol;
+        const long long cs = ncs;
         int32_t clo[RMAX], chi[RMAX];
 #pragma unroll
         for (int r = 0; r < RMAX; ++r) clo[r] = chi[r] = 0;
         if (e < e1) {
-          col = sidx[e];
-          const long long cs = (slab == 0) ? (long long)D.colsum[col] : 0;
 #pragma unroll
           for (int r = 0; r < RMAX; ++r) {
-            const long long C = act[r] ? __double2ll_rn(sc[e * R + r] * scale[r]) : 0;
+            const long long C = act[r] ? __double2ll_rn(nsc[r] * scale[r]) : 0;
             clo[r] = (int32_t)(C & 0x3FFFFF);
             chi[r] = (int32_t)(C >> 22);
             mt[r] += cs * C;
+          }
+        }
+        {
+          const int64_t en = e + 32;
+          if (en < e1) {
+            ncol = sidx[en];
+#pragma unroll
+            for (int r = 0; r < RMAX; ++r) nsc[r] = r < R ? sc[en * R + r] : 0.0;
           }
         }
         const int ng = (int)min((int64_t)32, e1 - g0);
@@ -229,6 +270,7 @@ __global__ void __launch_bounds__(KTHREADS) k1_bulk(const Dev D, int cur) {
             phase ^= 1;
           }
         }
+        if (slab == 0 && e + 32 < e1) ncs = (long long)D.colsum[ncol];
       }
       if (slab == 0) {
 #pragma unroll

@@ -25,10 +25,13 @@
 namespace {
 
 constexpr int KC = 32;         // support entries per chunk (one kind::i8 MMA K step)
-constexpr int THREADS = 256;   // w0 producer, w1 MMA, w2 TMEM alloc, w3 idle, w4-7 convert + epilogue
+// warps: 0 producer, 1 MMA, 2 TMEM alloc, 3 idle, 4..4+CW-1 convert + epilogue (CW/4 warps per
+// TMEM lane quarter, each taking every (CW/4)-th row tile: the byte-gather loop is latency-bound)
 
 template <int RMAX, int ST>
 struct K1T {
+  static constexpr int CW = 12;                                            // converter warps
+  static constexpr int THREADS = 32 * (4 + CW);
   static constexpr int NDIG = 6 * RMAX;                                    // digit columns in use
   static constexpr int N = NDIG <= 16 ? 16 : (NDIG <= 32 ? 32 : (NDIG <= 48 ? 48 : 96));
   static constexpr int RT = N <= 16 ? 16 : (N <= 32 ? 8 : (N <= 48 ? 4 : 2));   // row tiles per slab
@@ -85,11 +88,12 @@ __device__ __forceinline__ uint64_t umma_desc_kmajor_noswz(uint32_t saddr) {
 }
 
 template <int RMAX, int ST>
-__global__ void __launch_bounds__(THREADS, 1) k1_tc_kernel(const Dev D, int cur) {
+__global__ void __launch_bounds__(K1T<RMAX, ST>::THREADS, 1) k1_tc_kernel(const Dev D, int cur) {
   using T = K1T<RMAX, ST>;
+  constexpr int CW = T::CW, CG = CW / 4;
   constexpr int RT = T::RT, SR = T::SR, SEGB = T::SEGB, N = T::N, STAGES = T::STAGES, NAB = T::NAB;
   extern __shared__ uint8_t k1t_raw[];
-  uint8_t* sm = (uint8_t*)(((uintptr_t)k1t_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sm = k1t_raw + (((1023 + 1) - (smem_u32(k1t_raw) & 1023)) & 1023);
   uint8_t* sdata = sm;                                   // [STAGES][KC][SEGB]
   uint8_t* sB = sm + STAGES * KC * SEGB;                 // [STAGES][BTILE]
   uint64_t* full = (uint64_t*)(sm + STAGES * T::STAGE);
@@ -107,11 +111,11 @@ __global__ void __launch_bounds__(THREADS, 1) k1_tc_kernel(const Dev D, int cur)
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < NAB; ++a) {
-      mbar_init(&afull[a], 4);
+      mbar_init(&afull[a], CW);
       mbar_init(&aempty[a], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 4);
+    mbar_init(tempty, CW);
     fence_mbar_init();
   }
   if (wid == 2) {
@@ -162,21 +166,38 @@ __global__ void __launch_bounds__(THREADS, 1) k1_tc_kernel(const Dev D, int cur)
       long long mt[RMAX];
 #pragma unroll
       for (int r = 0; r < RMAX; ++r) mt[r] = 0;
+      // software pipeline: the entry (column, beta/s) loads of chunk i+1 and the colsum load of
+      // chunk i+1 are in flight while chunk i is written out
+      int32_t ncol = 0;
+      double nsc[RMAX];
+      long long ncs = 0;
+      {
+        const int64_t e = e0 + lane;
+        if (e < e1) {
+          ncol = sidx[e];
+#pragma unroll
+          for (int r = 0; r < RMAX; ++r) nsc[r] = r < R ? sc[e * R + r] : 0.0;
+          ncs = (slab == 0) ? (long long)D.colsum[ncol] : 0;
+        }
+      }
       for (int64_t g0 = e0; g0 < e1; g0 += KC) {
         const int64_t e = g0 + lane;
         const bool live = e < e1;
         const int ng = (int)min((int64_t)KC, e1 - g0);
-        int32_t col = 0;
+        const int32_t col = ncol;
+        const long long cs = ncs;
         long long C[RMAX];
 #pragma unroll
-        for (int r = 0; r < RMAX; ++r) C[r] = 0;
-        if (live) {
-          col = sidx[e];
-          const long long cs = (slab == 0) ? (long long)D.colsum[col] : 0;
+        for (int r = 0; r < RMAX; ++r) {
+          C[r] = (live && act[r]) ? __double2ll_rn(nsc[r] * scale[r]) : 0;
+          mt[r] += cs * C[r];
+        }
+        {
+          const int64_t en = e + KC;
+          if (en < e1) {
+            ncol = sidx[en];
 #pragma unroll
-          for (int r = 0; r < RMAX; ++r) {
-            C[r] = act[r] ? __double2ll_rn(sc[e * R + r] * scale[r]) : 0;
-            mt[r] += cs * C[r];
+            for (int r = 0; r < RMAX; ++r) nsc[r] = r < R ? sc[en * R + r] : 0.0;
           }
         }
         mbar_wait(&empty[stage], phase ^ 1);
@@ -198,6 +219,7 @@ __global__ void __launch_bounds__(THREADS, 1) k1_tc_kernel(const Dev D, int cur)
         if (lane == 0) mbar_expect_tx(&full[stage], bytes * (uint32_t)ng);
         __syncwarp();
         if (live) bulk_g2s(sdata + (stage * KC + lane) * SEGB, D.X8 + (int64_t)col * D.ld + boff, bytes, &full[stage], pol);
+        if (slab == 0 && e + KC < e1) ncs = (long long)D.colsum[ncol];
         if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
@@ -255,7 +277,7 @@ __global__ void __launch_bounds__(THREADS, 1) k1_tc_kernel(const Dev D, int cur)
     }
   } else if (wid >= 4) {
     // ===================== converters (TMEM lane quarter wid-4 = rows of every row tile) + epilogue
-    const int q4 = wid - 4;
+    const int q4 = wid & 3, h = (wid - 4) >> 2;   // lane quarter, row-tile subset
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     int stage = 0, ab = 0;
     uint32_t phase = 0, aphase = 0, tph = 0;
@@ -268,7 +290,7 @@ __global__ void __launch_bounds__(THREADS, 1) k1_tc_kernel(const Dev D, int cur)
         tc_fence_after();
         const uint8_t* sd = sdata + stage * KC * SEGB;
 #pragma unroll 1
-        for (int t = 0; t < RT; ++t) {
+        for (int t = h; t < RT; t += CG) {
           const int row = t * 128 + q4 * 32 + lane;   // row within the slab
           uint32_t wv[8];
 #pragma unroll
@@ -305,7 +327,7 @@ __global__ void __launch_bounds__(THREADS, 1) k1_tc_kernel(const Dev D, int cur)
       tph ^= 1;
       tc_fence_after();
 #pragma unroll 1
-      for (int t = 0; t < RT; ++t) {
+      for (int t = h; t < RT; t += CG) {
         const int row = slab * SR + t * 128 + q4 * 32 + lane;
         int32_t dv[N];
 #pragma unroll
@@ -347,9 +369,9 @@ cudaError_t init_one() {
 template <int RMAX>
 void launch_r(const Dev& D, int grid, cudaStream_t st, int cur) {
   if (D.storage == 1)
-    launch_pdl(k1_tc_kernel<RMAX, 1>, dim3(grid), dim3(THREADS), K1T<RMAX, 1>::SMEM, st, D, cur);
+    launch_pdl(k1_tc_kernel<RMAX, 1>, dim3(grid), dim3(K1T<RMAX, 1>::THREADS), K1T<RMAX, 1>::SMEM, st, D, cur);
   else
-    launch_pdl(k1_tc_kernel<RMAX, 2>, dim3(grid), dim3(THREADS), K1T<RMAX, 2>::SMEM, st, D, cur);
+    launch_pdl(k1_tc_kernel<RMAX, 2>, dim3(grid), dim3(K1T<RMAX, 2>::THREADS), K1T<RMAX, 2>::SMEM, st, D, cur);
 }
 
 }  // namespace

@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   using T = K1G<RMAX>;
   constexpr int RT = T::RT, SR = T::SR, N = T::N, STAGES = T::STAGES;
   extern __shared__ uint8_t k1g_raw[];
-  uint8_t* sm = (uint8_t*)(((uintptr_t)k1g_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sm = k1g_raw + (((1023 + 1) - (smem_u32(k1g_raw) & 1023)) & 1023);
   uint8_t* sA = sm;                                    // [STAGES][RT][4 KB]
   uint8_t* sB = sm + STAGES * RT * T::ATILE;           // [STAGES][BTILE]
   uint64_t* full = (uint64_t*)(sm + STAGES * T::STAGE);

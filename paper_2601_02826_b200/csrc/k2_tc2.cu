@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
   constexpr int THREADS = CF::THREADS;
   constexpr int EPI0 = 4 + CW;   // first epilogue warp
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = smem_raw + (((1023 + 1) - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* sA = smem;
   uint8_t* sB = smem + CF::STAGES * A_BYTES;
   uint64_t* full = (uint64_t*)(smem + CF::STAGES * CF::STAGE);

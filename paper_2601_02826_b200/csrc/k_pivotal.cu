@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     k_piv_kernel(const Dev D, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
                  const int* nb, unsigned long long* lmax) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = smem_raw + (((1023 + 1) - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
   uint64_t* full = (uint64_t*)(smem + STAGES * STAGE);
