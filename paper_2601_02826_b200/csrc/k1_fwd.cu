@@ -345,7 +345,9 @@ __global__ void __launch_bounds__(KTHREADS) k1_bulk(const Dev D, int cur) {
   }
 }
 
-// fp32 design: s_i = sum_j (x_ij - m_j) beta_j / s_j in ascending j (beta_0 added by finalize)
+// fp32 design: s_i = sum_j (x_ij - m_j) beta_j / s_j (beta_0 added by finalize).  Warp per row:
+// lane L takes the columns j = L, L+32, ... in ascending order (coalesced beta reads, X read only
+// for nonzero beta_j), then a fixed butterfly: deterministic for any launch.
 template <int RMAX>
 __global__ void __launch_bounds__(THREADS) k1_f32(const Dev D, int cur) {
   pdl_launch_dependents();
@@ -354,11 +356,13 @@ __global__ void __launch_bounds__(THREADS) k1_f32(const Dev D, int cur) {
   const long long k = *D.iter;
   const double* beta = D.beta[(int)((k + (cur ? 0 : 1)) & 1)];
   const int R = D.R;
-  for (int i = blockIdx.x * THREADS + threadIdx.x; i < D.n; i += gridDim.x * THREADS) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * THREADS) >> 5;
+  for (int64_t i = ((int64_t)blockIdx.x * THREADS + threadIdx.x) >> 5; i < D.n; i += nw) {
     double a[RMAX];
 #pragma unroll
     for (int r = 0; r < RMAX; ++r) a[r] = 0.0;
-    for (int64_t c = 0; c < D.p; ++c) {
+    for (int64_t c = lane; c < D.p; c += 32) {
       const double* bj = beta + (c + 1) * R;
       bool any = false;
 #pragma unroll
@@ -372,8 +376,10 @@ __global__ void __launch_bounds__(THREADS) k1_f32(const Dev D, int cur) {
         if (r < R) a[r] = fma(x, bj[r] * isd, a[r]);
     }
 #pragma unroll
-    for (int r = 0; r < RMAX; ++r)
-      if (r < R && (cur || D.status[r] == ST_ACTIVE)) D.sdense[(int64_t)r * D.n + i] = a[r];
+    for (int r = 0; r < RMAX; ++r) {
+      const double v = warp_sum_d(a[r]);
+      if (lane == 0 && r < R && (cur || D.status[r] == ST_ACTIVE)) D.sdense[(int64_t)r * D.n + i] = v;
+    }
   }
 }
 
@@ -387,7 +393,7 @@ int bulk_grid(int grid) {
 template <int RMAX>
 void launch_r(const Dev& D, int grid, cudaStream_t st, int cur) {
   if (D.storage == 0)
-    launch_pdl(k1_f32<RMAX>, dim3((D.n + THREADS - 1) / THREADS), dim3(THREADS), 0, st, D, cur);
+    launch_pdl(k1_f32<RMAX>, dim3((D.n + THREADS / 32 - 1) / (THREADS / 32)), dim3(THREADS), 0, st, D, cur);
   else if (D.storage == 1)
     launch_pdl(k1_bulk<RMAX, 1>, dim3(bulk_grid<RMAX, 1>(grid)), dim3(KTHREADS), K1Smem<RMAX, 1>::BYTES, st, D, cur);
   else

@@ -134,7 +134,7 @@ def run(name, args):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="c2,c3,c4,c5,m")
+    ap.add_argument("--configs", default="c1,c2,c3,c4,c5,m")
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--burn-in", dest="burn_in", type=int, default=200)
     ap.add_argument("--tol", type=float, default=1e-4)
