@@ -26,8 +26,8 @@ Parity status per function (DESIGN.md §4 repeats this table):
                   E[(x~_j^T psi)^2] = tau(1-tau)(n-1) (law of large numbers), invariance to
                   genotype recoding 2-x and to column order; a hand-built 3x2 case
   hbic            pinned: SPEC worked value and the closed form on a null model
-  trajectory after k iterations: parity unpinned beyond the composition of pinned steps
-                  (the paper prints no iterates); see DESIGN.md §4.
+  trajectory      pinned: Theorem 1's Fejer monotonicity in the H-norm on every step of 300-step
+                  trajectories (the paper prints no iterates); see DESIGN.md §4.
 """
 from __future__ import annotations
 
