@@ -213,6 +213,11 @@ fsqr_status fsqr_get_colstats(fsqr_ctx* ctx, double* mean_host, double* sd_host)
 fsqr_status fsqr_path(fsqr_ctx* ctx, const double* lam_path_host, int32_t T, int64_t* total, int64_t* iters_host,
                       double* obj_host, double* R_host, int64_t* nnz_host, int32_t* converged_host, void* stream);
 
+/* HBIC (E18, L408-411) of every recorded path point, hbic_host [n_rhs][T]: log(sum_i rho_tau) +
+ * |A| (log log n / n) log p at the recorded iterate (the paper's lambda selection in sparse
+ * settings, L406-411).  FSQR_ERR_STATE before fsqr_path. */
+fsqr_status fsqr_path_hbic(fsqr_ctx* ctx, double* hbic_host);
+
 /* Sparse solution of path point t for RHS r: writes up to cap (index j, beta_j standardised) pairs,
  * returns the count in *count (which may exceed cap: then only cap were written). */
 fsqr_status fsqr_path_beta(fsqr_ctx* ctx, int32_t r, int32_t t, int64_t cap, int64_t* idx_host, double* beta_host,

@@ -56,7 +56,7 @@ class fsqr_result(ctypes.Structure):
 EXPORTS = ["fsqr_default_options", "fsqr_create", "fsqr_iterate", "fsqr_solve", "fsqr_objective", "fsqr_kkt",
            "fsqr_get_beta", "fsqr_get_state", "fsqr_set_state", "fsqr_set_lambda", "fsqr_lambda_max",
            "fsqr_get_eta", "fsqr_get_colstats", "fsqr_path", "fsqr_path_beta", "fsqr_trace", "fsqr_iterations",
-           "fsqr_profile_iterate", "fsqr_hbic", "fsqr_set_lambda_weights", "fsqr_lla", "fsqr_pivotal", "fsqr_set_lambda2",
+           "fsqr_profile_iterate", "fsqr_hbic", "fsqr_set_lambda_weights", "fsqr_lla", "fsqr_pivotal", "fsqr_set_lambda2", "fsqr_path_hbic",
            "fsqr_backend_name", "fsqr_fit_host", "fsqr_last_error", "fsqr_global_error", "fsqr_status_str",
            "fsqr_destroy"]
 
@@ -103,6 +103,7 @@ def load(build_if_missing: bool = True):
     L.fsqr_profile_iterate.restype = S
     L.fsqr_hbic.argtypes = [ctxp, P, P]
     L.fsqr_set_lambda2.argtypes = [ctxp, P]
+    L.fsqr_path_hbic.argtypes = [ctxp, P]
     L.fsqr_pivotal.argtypes = [ctxp, I32, I64, ctypes.c_uint64, P, P]
     L.fsqr_set_lambda_weights.argtypes = [ctxp, P, P]
     L.fsqr_lla.argtypes = [ctxp, I32, D, I32, P, ctypes.POINTER(fsqr_result), P]
@@ -123,7 +124,7 @@ def load(build_if_missing: bool = True):
     for name in ("fsqr_create", "fsqr_iterate", "fsqr_solve", "fsqr_objective", "fsqr_kkt", "fsqr_get_beta",
                  "fsqr_get_state", "fsqr_set_state", "fsqr_set_lambda", "fsqr_lambda_max", "fsqr_get_eta",
                  "fsqr_get_colstats", "fsqr_path", "fsqr_path_beta", "fsqr_trace", "fsqr_fit_host", "fsqr_hbic",
-                 "fsqr_set_lambda_weights", "fsqr_lla", "fsqr_pivotal", "fsqr_set_lambda2"):
+                 "fsqr_set_lambda_weights", "fsqr_lla", "fsqr_pivotal", "fsqr_set_lambda2", "fsqr_path_hbic"):
         getattr(L, name).restype = S
     _lib = L
     return L
@@ -263,6 +264,12 @@ def fsqr_path(ctx, lam_path, stream=None) -> dict:
     _check(load().fsqr_path(ctx, _ptr(lp), T, ctypes.byref(total), _ptr(it), _ptr(obj), _ptr(RR), _ptr(nnz),
                             _ptr(conv), _stream(stream)), ctx)
     return dict(total=total.value, iters=it, obj=obj, R=RR, nnz=nnz, converged=conv.astype(bool))
+
+
+def fsqr_path_hbic(ctx, n_rhs: int, T: int) -> np.ndarray:
+    out = np.empty((n_rhs, T))
+    _check(load().fsqr_path_hbic(ctx, _ptr(out)), ctx)
+    return out
 
 
 def fsqr_path_beta(ctx, r: int, t: int, p: int) -> np.ndarray:
@@ -417,6 +424,28 @@ class Solver:
 
     def path(self, lam_path):
         return fsqr_path(self.ctx, lam_path)
+
+    def path_hbic(self, T: int):
+        return fsqr_path_hbic(self.ctx, self.R, T)
+
+    def tune(self, T: int = 50, lam_min_frac: float = 0.01, B: int = 0, seed: int = 0x5EED):
+        """The paper's tuning protocol for sparse settings (L406-412) on the GPU: a warm-started
+        geometric lambda path of T points per tau, from lambda_max (or, with B > 0 replicates, from
+        the pivotal lambda of reading R18 up to lambda_max) down to lam_min_frac times its top,
+        HBIC (E18) of every point, and the minimiser.  Returns dict(grid, hbic, best, beta)."""
+        lm = np.asarray(self.lambda_max())
+        top = lm.copy()
+        if B > 0:
+            for r in range(self.R):
+                L = fsqr_pivotal(self.ctx, r, B, seed)
+                s = np.sort(L)
+                top[r] = max(lm[r], 1.1 * s[int(np.ceil(0.9 * B)) - 1])
+        grid = np.array([[top[r] * lam_min_frac ** (t / (T - 1)) for t in range(T)] for r in range(self.R)])
+        res = self.path(grid)
+        h = self.path_hbic(T)
+        best = np.argmin(h, axis=1)
+        beta = np.stack([self.path_beta(r, int(best[r])) for r in range(self.R)])
+        return dict(grid=grid, path=res, hbic=h, best=best, beta=beta)
 
     def path_beta(self, r: int, t: int):
         return fsqr_path_beta(self.ctx, r, t, self.p)

@@ -1089,6 +1089,20 @@ fsqr_status fsqr_path(fsqr_ctx* ctx, const double* lam_path_host, int32_t T, int
   return FSQR_OK;
 }
 
+fsqr_status fsqr_path_hbic(fsqr_ctx* ctx, double* hbic_host) {
+  if (!ctx || !hbic_host) return set_err(ctx, FSQR_ERR_CONFIG, "null argument");
+  if (!ctx->D.path_rec) return set_err(ctx, FSQR_ERR_STATE, "fsqr_path has not run");
+  const int R = ctx->R, T = ctx->T;
+  std::vector<double> rec((size_t)R * T * FSQR_PATH_W);
+  CK(cudaMemcpy(rec.data(), ctx->D.path_rec, sizeof(double) * rec.size(), cudaMemcpyDeviceToHost));
+  const double n = (double)ctx->n, p = (double)ctx->p;
+  for (int64_t q = 0; q < (int64_t)R * T; ++q) {
+    const double* pr = &rec[q * FSQR_PATH_W];
+    hbic_host[q] = std::log(pr[7]) + pr[5] * (std::log(std::log(n)) / n) * std::log(p);
+  }
+  return FSQR_OK;
+}
+
 fsqr_status fsqr_path_beta(fsqr_ctx* ctx, int32_t r, int32_t t, int64_t cap, int64_t* idx_host, double* beta_host,
                            int64_t* count) {
   if (!ctx || !count) return set_err(ctx, FSQR_ERR_CONFIG, "null argument");

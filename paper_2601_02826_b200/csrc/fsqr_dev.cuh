@@ -24,7 +24,7 @@
 #define FSQR_FPART 8          // finalize partials per CTA and RHS: 7 sums + max|theta|
 #define FIN_THREADS 256
 #define FIN_MAXGRID 256       // ceil(65536 / FIN_THREADS)
-#define FSQR_PATH_W 7         // path record: iters, Rp, Rb, Rz, obj, nnz, converged
+#define FSQR_PATH_W 8         // path record: iters, Rp, Rb, Rz, obj, nnz, converged, loss sum
 
 enum { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_NUMERIC = 3 };
 

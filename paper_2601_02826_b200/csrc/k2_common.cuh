@@ -122,6 +122,7 @@ __device__ void k2_finish(const Dev& D, const K2Ctx<RMAX>& C, K2Part<RMAX>& P, d
             pr[4] = obj;
             pr[5] = a[4];
             pr[6] = conv ? 1.0 : 0.0;
+            pr[7] = sc[2];   // sum_i rho_tau(y_i - x~_i^T beta^k): HBIC of the point (E18)
             s_rec[r] = t;
             if (t == D.T - 1) {
               D.status[r] = conv ? ST_CONVERGED : ST_MAXITER;

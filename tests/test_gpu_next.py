@@ -139,3 +139,25 @@ def test_elastic_net_matches_oracle(cuda_ok, storage, lam2):
     bb = S.beta()[0]
     assert rel(bb, oc["beta"]) < 1e-4
     assert S.objective()[0] == pytest.approx(oracle.objective_en(d, prob.y, c["tau"], lv, lam2, oc["beta"]), rel=1e-4)
+
+
+def test_path_hbic_and_tune_match_oracle(cuda_ok):
+    """The paper's sparse-setting tuning (L406-412): warm-started geometric path, HBIC (E18) per
+    point, argmin.  HBIC of every recorded point equals the oracle's HBIC of the oracle's point."""
+    import paper_2601_02826_b200 as fs
+
+    prob = datagen.make("c2", n=600, p=1200)
+    d = oracle.Design.from_problem(prob)
+    tau, G, T, tol = 0.5, 5, 8, 1e-5
+    mu = 2.0 / prob.n
+    eta = oracle.eta(d, G, mu)
+    X, y = to_device(prob)
+    S = fs.Solver(X, prob.storage, prob.n, prob.p, prob.ld, y, [tau], [1.0], G=G, mu=mu, eta=eta, tol=tol,
+                  max_iter_point=5000)
+    out = S.tune(T=T, lam_min_frac=0.05)
+    grid = out["grid"][0]
+    o = oracle.path(d, prob.y, tau, grid, eta, mu, G, tol, 5000)
+    ho = np.array([oracle.hbic(d, prob.y, tau, o["beta_path"][t]) for t in range(T)])
+    np.testing.assert_allclose(out["hbic"][0], ho, rtol=1e-6)
+    assert out["best"][0] == int(np.argmin(ho))
+    assert rel(out["beta"][0], o["beta_path"][int(np.argmin(ho))]) < 1e-4
