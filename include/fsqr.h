@@ -223,8 +223,9 @@ fsqr_status fsqr_path_hbic(fsqr_ctx* ctx, double* hbic_host);
 fsqr_status fsqr_path_beta(fsqr_ctx* ctx, int32_t r, int32_t t, int64_t cap, int64_t* idx_host, double* beta_host,
                            int64_t* count);
 
-/* Per-iteration trace [min(k, trace_cap)][n_rhs][5] = (R_p, R_beta, R_z, objective, |support|) of w^k
- * for the last iterations, oldest first; returns rows written in *rows. */
+/* Per-iteration trace [rows][n_rhs][5] = (R_p, R_beta, R_z, objective, |support|) of w^k for the
+ * last min(k_last + 1, trace_cap, cap_rows) iterates k, oldest first (after a stop, the last row is
+ * the iterate that passed the test); returns rows written in *rows. */
 fsqr_status fsqr_trace(fsqr_ctx* ctx, double* out_host, int64_t cap_rows, int64_t* rows);
 
 /* Measurement entry: run exactly k iterations like fsqr_iterate but as individual launches with

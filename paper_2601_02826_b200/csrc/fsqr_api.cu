@@ -1125,7 +1125,10 @@ fsqr_status fsqr_path_beta(fsqr_ctx* ctx, int32_t r, int32_t t, int64_t cap, int
 fsqr_status fsqr_trace(fsqr_ctx* ctx, double* out_host, int64_t cap_rows, int64_t* rows) {
   if (!ctx || !out_host || !rows) return set_err(ctx, FSQR_ERR_CONFIG, "null argument");
   long long it = 0;
+  int stopped = 0;
   CK(cudaMemcpy(&it, ctx->D.iter, sizeof it, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&stopped, ctx->D.stop, sizeof stopped, cudaMemcpyDeviceToHost));
+  if (stopped) ++it;   // the pass that found R(w^k) <= tol wrote row k before the iteration stopped
   const int W = ctx->R * FSQR_TRACE_W;
   std::vector<double> tr((size_t)ctx->opt.trace_cap * W);
   CK(cudaMemcpy(tr.data(), ctx->D.trace, sizeof(double) * tr.size(), cudaMemcpyDeviceToHost));
