@@ -129,3 +129,20 @@ def test_converged_parity_c2_tau09(cuda_ok):
     assert np.array_equal(b != 0, o["beta"] != 0)
     _, z, t = S.state()
     assert oracle.kkt_rel(d, prob.y, 0.9, lv, b, z[0], t[0]).max() < 2e-6
+
+
+@pytest.mark.parametrize("storage", [1, 2])
+def test_unpenalised_full_support(cuda_ok, storage):
+    """lambda = 0 with p + 1 < n: classical quantile regression (Koenker-Bassett, L57); every
+    column is in the support, so the forward product streams all of X; the converged objective
+    equals the oracle's."""
+    name = "c2" if storage == 1 else "c4"
+    prob, d, S, cfg = make_pair(name, n=300, p=12, storage=storage, G=2, taus=[0.35], lam_frac=0.0, tol=1e-7,
+                                max_iter=400000)
+    res = S.solve()
+    assert res["status"] == 0, res
+    o = oracle.solve(d, prob.y, 0.35, oracle.lam_vector(prob.p, 0.0), cfg["eta"], cfg["mu"], 2, max_iter=400000,
+                     tol=1e-7)
+    assert o["status"] == 0
+    assert np.count_nonzero(S.beta()[0][1:]) == prob.p
+    assert S.objective()[0] == pytest.approx(o["obj"], rel=1e-6)
