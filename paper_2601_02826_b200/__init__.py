@@ -62,7 +62,7 @@ EXPORTS = ["fsqr_default_options", "fsqr_create", "fsqr_iterate", "fsqr_solve", 
 
 
 def lib_path() -> str:
-    return _build.LIB
+    return os.environ.get("FSQR_LIB", _build.LIB)   # FSQR_LIB: an alternative build, for measurements
 
 
 def load(build_if_missing: bool = True):
@@ -78,7 +78,7 @@ def load(build_if_missing: bool = True):
                 raise RuntimeError(f"libfsqr.so missing and cannot be built: {e}") from e
     if not os.path.exists(_build.LIB):
         raise RuntimeError("libfsqr.so is missing: run paper_2601_02826_b200._build.build()")
-    L = ctypes.CDLL(_build.LIB)
+    L = ctypes.CDLL(lib_path())
     P, I32, I64, D, S = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_int
     ctxp = ctypes.c_void_p
     L.fsqr_default_options.argtypes = [ctypes.POINTER(fsqr_options)]

@@ -21,6 +21,16 @@
 
 namespace {
 
+#ifndef K1_SMEM_KB
+#define K1_SMEM_KB 96   // stage-ring budget per CTA (two CTAs per SM)
+#endif
+#ifndef K1_RPT1
+#define K1_RPT1 8       // rows per consumer thread for one RHS
+#endif
+#ifndef K1_QC_BIG
+#define K1_QC_BIG 8     // columns per stage for 2 KB segments
+#endif
+
 constexpr int THREADS = 256;
 constexpr int NCW = 8;              // consumer warps
 constexpr int KTHREADS = 32 * (NCW + 1);
@@ -33,11 +43,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // rows per thread: keep 4 * RPT * RMAX int32-equivalent accumulator registers <= 64
-// (measured at M: 16 rows per thread / 4 KB copies was slower (58 vs 53 us); an fp64
-// one-DFMA-per-element variant ran the same 53 us as the two-IMAD one)
+// (measured at M: 16 rows per thread / 4 KB copies was slower (58-61 vs 52 us); an fp64
+// one-DFMA-per-element variant ran the same 53 us as the two-IMAD one; 2, 3 or 4 CTAs per SM
+// (96 / 64 / 48 KB rings) all ran 52 us; 16 columns per stage 65 us)
 template <int RMAX, int ST>
 struct K1Shape {
-  static constexpr int RPT = RMAX <= 2 ? 8 : (RMAX <= 4 ? 4 : (RMAX <= 8 ? 2 : 1));
+  static constexpr int RPT = RMAX == 1 ? K1_RPT1 : (RMAX <= 2 ? 8 : (RMAX <= 4 ? 4 : (RMAX <= 8 ? 2 : 1)));
   static constexpr int RPW = 256 * RPT;
 };
 
@@ -125,12 +136,13 @@ __device__ __forceinline__ void consume_col(const uint8_t* seg, const int32_t* c
   }
 }
 
+
 template <int RMAX, int ST>
 struct K1Smem {
   static constexpr int RPT = K1Shape<RMAX, ST>::RPT;
   static constexpr int SEG = ST == 1 ? 256 * RPT : 64 * RPT;   // bytes of one column's slab segment
-  static constexpr int QC = SEG >= 2048 ? 8 : (SEG >= 1024 ? 16 : 32);   // columns per stage (divides 32)
-  static constexpr int ST0 = (96 * 1024) / (QC * SEG);
+  static constexpr int QC = SEG >= 2048 ? K1_QC_BIG : (SEG >= 1024 ? 16 : 32);   // columns per stage (divides 32)
+  static constexpr int ST0 = (K1_SMEM_KB * 1024) / (QC * SEG);
   static constexpr int STAGES = ST0 < 4 ? 4 : (ST0 > 12 ? 12 : ST0);
   static constexpr int DATA = STAGES * QC * SEG;
   static constexpr int COEF = STAGES * QC * RMAX * 2 * 4;      // int32 lo/hi per slot and RHS
