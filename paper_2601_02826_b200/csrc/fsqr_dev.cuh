@@ -330,60 +330,89 @@ struct K2Ctx {
   const K2Const<RMAX>* cs;  // shared memory
 };
 
-// per-thread fp64 partials
+// fp64 partials of the stopping test: per thread in registers for up to 4 RHS; for 5+ RHS the
+// registers would spill the epilogue, so every column's contributions are warp-reduced at once
+// and added by lane 0 to this warp's slot [RMAX][NPART+1] of the CTA reduction buffer (fixed
+// order: deterministic).  In that mode epi_column must be called by all 32 lanes.
 template <int RMAX>
 struct K2Part {
-  double v[RMAX][FSQR_NPART];
-  double cmax[RMAX];
+  static constexpr bool SM = RMAX > 4;
+  double v[SM ? 1 : RMAX][FSQR_NPART];
+  double cmax[SM ? 1 : RMAX];
+  double* slot;   // SM mode: red + wid * RMAX * (NPART + 1)
   __device__ __forceinline__ void zero() {
 #pragma unroll
-    for (int r = 0; r < RMAX; ++r) {
+    for (int r = 0; r < (SM ? 1 : RMAX); ++r) {
       cmax[r] = 0.0;
 #pragma unroll
       for (int q = 0; q < FSQR_NPART; ++q) v[r][q] = 0.0;
     }
   }
+  __device__ __forceinline__ void add(int r, const double (&x)[FSQR_NPART], double cm) {
+    if constexpr (SM) {
+      constexpr int W = FSQR_NPART + 1;
+#pragma unroll
+      for (int q = 0; q < FSQR_NPART; ++q) {
+        const double t = warp_sum_d(x[q]);
+        if ((threadIdx.x & 31) == 0) slot[r * W + q] += t;
+      }
+      double m = cm;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if ((threadIdx.x & 31) == 0) slot[r * W + FSQR_NPART] = fmax(slot[r * W + FSQR_NPART], m);
+    } else {
+#pragma unroll
+      for (int q = 0; q < FSQR_NPART; ++q) v[r][q] += x[q];
+      cmax[r] = fmax(cmax[r], cm);
+    }
+  }
 };
 
-// a2 epilogue for one data column c with g_r = (X~^T theta^k)_j, j = c + 1.
+// a2 epilogue for one data column c with g_r = (X~^T theta^k)_j, j = c + 1 (valid lanes only;
+// invalid lanes contribute zeros -- all lanes must call it when K2Part is in shared-memory mode).
 // Writes beta^{k+1}, accumulates R_beta(w^k) partials and the penalty of beta^k,
 // returns whether beta^{k+1}_j != 0 for some active RHS (support membership) and
 // fills cval/bval for the support entry.
 template <int RMAX>
 __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, int64_t c, const double* g,
-                                           K2Part<RMAX>& P, double* cval, double* bval) {
+                                           K2Part<RMAX>& P, double* cval, double* bval, bool valid = true) {
   const int64_t j = c + 1;
-  const double isd = D.inv_sd[c];
-  const double eta = D.eta[block_of_col(D, j)];
+  const double isd = valid ? D.inv_sd[c] : 0.0;
+  const double eta = valid ? D.eta[block_of_col(D, j)] : 1.0;
   bool nz = false;
 #pragma unroll
   for (int r = 0; r < RMAX; ++r) {
     cval[r] = 0.0;
     bval[r] = 0.0;
-    if (r >= C.R || !C.cs->active[r]) continue;
-    const double b = C.beta_in[j * C.R + r];
-    const double lam = C.use_w ? C.cs->lam[r] * D.lamw[j * C.R + r] : C.cs->lam[r];
-    // KKT residual part of w^k and penalty at beta^k
-    const double l2 = C.cs->lam2[r];
-    const double d = b - soft_thr(b + (g[r] - l2 * b), lam);   // KKT: g - lam2 b in lam d|b|
-    P.v[r][0] += d * d;
-    P.v[r][1] += b * b;
-    P.v[r][2] += g[r] * g[r];
-    P.v[r][3] += lam * fabs(b) + 0.5 * l2 * b * b;
-    P.v[r][4] += (b != 0.0) ? 1.0 : 0.0;
-    if (D.update) {
-      // E14, or the elastic-net block prox (Remark 3, L347-349; reading R19) when lam2 > 0
-      const double bn = l2 == 0.0 ? prox_beta(b, g[r], lam, eta)
-                                  : (pos_part(eta * b + g[r] - lam) - pos_part(-eta * b - g[r] - lam)) / (eta + l2);
-      C.beta_out[j * C.R + r] = bn;
-      if (bn != 0.0) {
-        nz = true;
-        const double cv = bn * isd;
-        cval[r] = cv;
-        bval[r] = bn;
-        P.cmax[r] = fmax(P.cmax[r], fabs(cv));
+    if (r >= C.R || !C.cs->active[r]) continue;   // warp-uniform
+    double x[FSQR_NPART] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    double cm = 0.0;
+    if (valid) {
+      const double b = C.beta_in[j * C.R + r];
+      const double lam = C.use_w ? C.cs->lam[r] * D.lamw[j * C.R + r] : C.cs->lam[r];
+      // KKT residual part of w^k and penalty at beta^k
+      const double l2 = C.cs->lam2[r];
+      const double d = b - soft_thr(b + (g[r] - l2 * b), lam);   // KKT: g - lam2 b in lam d|b|
+      x[0] = d * d;
+      x[1] = b * b;
+      x[2] = g[r] * g[r];
+      x[3] = lam * fabs(b) + 0.5 * l2 * b * b;
+      x[4] = (b != 0.0) ? 1.0 : 0.0;
+      if (D.update) {
+        // E14, or the elastic-net block prox (Remark 3, L347-349; reading R19) when lam2 > 0
+        const double bn = l2 == 0.0 ? prox_beta(b, g[r], lam, eta)
+                                    : (pos_part(eta * b + g[r] - lam) - pos_part(-eta * b - g[r] - lam)) / (eta + l2);
+        C.beta_out[j * C.R + r] = bn;
+        if (bn != 0.0) {
+          nz = true;
+          const double cv = bn * isd;
+          cval[r] = cv;
+          bval[r] = bn;
+          cm = fabs(cv);
+        }
       }
     }
+    P.add(r, x, cm);
   }
   return nz;
 }

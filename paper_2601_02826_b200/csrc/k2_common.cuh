@@ -32,22 +32,36 @@ __device__ void k2_load_ctx(const Dev& D, K2Ctx<RMAX>& C) {
 // Block reduction of the per-thread partials (fixed order), publication of the
 // CTA partials, and, in the last CTA to finish, the a6 test.  Must be called by
 // every thread of the block; `red` needs blockDim/32 * RMAX * (NPART+1) doubles.
+// zero the reduction buffer and point a shared-memory-mode K2Part at this warp's slot (all threads,
+// before k2_load_ctx, whose block barrier orders the zeroing before any epilogue add)
+template <int RMAX>
+__device__ __forceinline__ void k2_part_init(K2Part<RMAX>& P, double* red) {
+  P.zero();
+  if constexpr (K2Part<RMAX>::SM) {
+    const int nw = blockDim.x >> 5;
+    for (int q = threadIdx.x; q < nw * RMAX * (FSQR_NPART + 1); q += blockDim.x) red[q] = 0.0;
+    P.slot = red + (threadIdx.x >> 5) * RMAX * (FSQR_NPART + 1);
+  }
+}
+
 template <int RMAX>
 __device__ void k2_finish(const Dev& D, const K2Ctx<RMAX>& C, K2Part<RMAX>& P, double* red) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
   constexpr int W = FSQR_NPART + 1;
+  if constexpr (!K2Part<RMAX>::SM) {   // shared-memory mode: the per-warp slots are already in red
 #pragma unroll
-  for (int r = 0; r < RMAX; ++r) {
-    if (r >= C.R) break;
+    for (int r = 0; r < RMAX; ++r) {
+      if (r >= C.R) break;
 #pragma unroll
-    for (int q = 0; q < FSQR_NPART; ++q) {
-      double v = warp_sum_d(P.v[r][q]);
-      if (lane == 0) red[(wid * RMAX + r) * W + q] = v;
+      for (int q = 0; q < FSQR_NPART; ++q) {
+        double v = warp_sum_d(P.v[r][q]);
+        if (lane == 0) red[(wid * RMAX + r) * W + q] = v;
+      }
+      double m = P.cmax[r];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) red[(wid * RMAX + r) * W + FSQR_NPART] = m;
     }
-    double m = P.cmax[r];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) red[(wid * RMAX + r) * W + FSQR_NPART] = m;
   }
   __syncthreads();
   __shared__ bool s_last;

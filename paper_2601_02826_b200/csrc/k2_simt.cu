@@ -29,10 +29,10 @@ __global__ void __launch_bounds__(THREADS) k2_simt_int(const Dev D) {
   pdl_launch_dependents();
   pdl_wait();
   if (*D.stop) return;
+  K2Part<RMAX> P;
+  k2_part_init(P, red);
   K2Ctx<RMAX> C;
   k2_load_ctx(D, C);
-  K2Part<RMAX> P;
-  P.zero();
   const int lane = threadIdx.x & 31;
   const int64_t gw = (int64_t)blockIdx.x * (THREADS / 32) + (threadIdx.x >> 5);
   const int64_t nwarps = (int64_t)gridDim.x * (THREADS / 32);
@@ -95,15 +95,27 @@ __global__ void __launch_bounds__(THREADS) k2_simt_int(const Dev D) {
 #pragma unroll
     for (int a = 0; a < CPW; ++a) {
       const int64_t c = grp * CPW + a;
-      if (lane == a && c < D.p) {
+      const bool valid = lane == a && c < D.p;
+      double g[RMAX];
+#pragma unroll
+      for (int r = 0; r < RMAX; ++r) g[r] = 0.0;
+      if (valid) {
         cc = c;
-        double g[RMAX];
         const int32_t cs = D.colsum[c];
         const double isd = D.inv_sd[c];
 #pragma unroll
         for (int r = 0; r < RMAX; ++r)
           g[r] = r < C.R ? g_from_digits(D.n, cs, C.cs->Tsum[r], C.cs->gscale[r], isd, &acc[a][4 * r]) : 0.0;
-        nz = epi_column<RMAX>(D, C, c, g, P, cval, bval);
+      }
+      double cv2[RMAX], bv2[RMAX];
+      const bool z2 = epi_column<RMAX>(D, C, valid ? c : 0, g, P, cv2, bv2, valid);
+      if (valid) {
+        nz = z2;
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r) {
+          cval[r] = cv2[r];
+          bval[r] = bv2[r];
+        }
       }
     }
     if (D.update) support_append<RMAX>(C, nz, cc, cval, bval);
@@ -118,10 +130,10 @@ __global__ void __launch_bounds__(THREADS) k2_simt_f32(const Dev D) {
   pdl_launch_dependents();
   pdl_wait();
   if (*D.stop) return;
+  K2Part<RMAX> P;
+  k2_part_init(P, red);
   K2Ctx<RMAX> C;
   k2_load_ctx(D, C);
-  K2Part<RMAX> P;
-  P.zero();
   const int lane = threadIdx.x & 31;
   const int64_t gw = (int64_t)blockIdx.x * (THREADS / 32) + (threadIdx.x >> 5);
   const int64_t nwarps = (int64_t)gridDim.x * (THREADS / 32);
@@ -145,7 +157,7 @@ __global__ void __launch_bounds__(THREADS) k2_simt_f32(const Dev D) {
     double cval[RMAX], bval[RMAX];
 #pragma unroll
     for (int r = 0; r < RMAX; ++r) cval[r] = bval[r] = 0.0;
-    if (lane == 0) nz = epi_column<RMAX>(D, C, c, g, P, cval, bval);
+    nz = epi_column<RMAX>(D, C, c, g, P, cval, bval, lane == 0);
     if (D.update) support_append<RMAX>(C, nz, c, cval, bval);
   }
   __syncthreads();

@@ -165,10 +165,10 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
     }
     return;
   }
+  K2Part<RMAX> P;
+  k2_part_init(P, red);
   K2Ctx<RMAX> C;
   k2_load_ctx(D, C);
-  K2Part<RMAX> P;
-  P.zero();
 
   if (wid == 0) {
     // ===== TMA producer: the whole warp walks the ring, one elected lane issues =====
@@ -330,20 +330,20 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
       if (lane == 0) mbar_arrive(&tempty[acc]);
 
       const int64_t c = t * TILE_M + q * 32 + lane;
-      bool nz = false;
-      double cval[RMAX], bval[RMAX];
-      if (c < D.p) {
-        double g[RMAX];
+      const bool valid = c < D.p;
+      double g[RMAX];
+      if (valid) {
         const int32_t cs = D.colsum[c];
         const double isd = D.inv_sd[c];
 #pragma unroll
         for (int r = 0; r < RMAX; ++r)
           g[r] = r < C.R ? g_from_digits(D.n, cs, C.cs->Tsum[r], C.cs->gscale[r], isd, dv + 4 * r) : 0.0;
-        nz = epi_column<RMAX>(D, C, c, g, P, cval, bval);
       } else {
 #pragma unroll
-        for (int r = 0; r < RMAX; ++r) cval[r] = bval[r] = 0.0;
+        for (int r = 0; r < RMAX; ++r) g[r] = 0.0;
       }
+      double cval[RMAX], bval[RMAX];
+      const bool nz = epi_column<RMAX>(D, C, valid ? c : 0, g, P, cval, bval, valid);
       if (D.update) support_append<RMAX>(C, nz, c, cval, bval);
     }
   }
