@@ -218,8 +218,10 @@ def run_ours(args):
 
     # setup (a0, a0', lambda_max) timed separately; lambda = frac * lambda_max from the GPU
     t0 = time.perf_counter()
+    pack = args.storage == "pack2" and prob.storage == fs.U8
+    flags = fs.DESIGN_PACK2 if pack else 0
     S = fs.Solver(Xd, prob.storage, prob.n, prob.p, prob.ld, yd, [tau], [1.0], G=G, mu=mu, tol=args.kkt_tol,
-                  max_iter=args.kkt_max_iter)
+                  max_iter=args.kkt_max_iter, flags=flags)
     lm = float(S.lambda_max()[0])
     S.set_lambda([prob.lam_frac * lm])
     t_setup = time.perf_counter() - t0
@@ -253,16 +255,32 @@ def run_ours(args):
     stage_ms, prof_total_ms = fs.fsqr_profile_iterate(S.ctx, args.steps)
 
     # roofline of the dominant kernel (K2: X~^T theta + beta prox), algorithmic bytes per launch
-    xbytes = prob.n * prob.p                        # every stored genotype byte, read once
+    xbytes = prob.n * prob.p // (4 if pack else 1)  # every genotype code (1 byte, or 2 bits packed), read once
     state_bytes = 28 * prob.p                       # beta r/w (16 B) + colsum (4 B) + 1/s_j (8 B) per column
     k2_ms = stage_ms[0] / k
     peak, peak_kind = peaks()
     achieved = (xbytes + state_bytes) / (k2_ms / 1000.0) / 1e9
-    traffic = k2_traffic(args.config)
+    traffic = k2_traffic(args.config + ("_pack2" if pack else ""))
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "kernel": f"k2_{S.backend}", "peak_source": peak_kind,
             "algorithmic_bytes_per_launch": xbytes + state_bytes,
             "kernel_share_of_step": stage_ms[0] / prof_total_ms}
+
+    # the same iterations with the u8 codes streamed as stored (no repack), for comparison
+    u8_line = None
+    if pack:
+        S8 = fs.Solver(Xd, prob.storage, prob.n, prob.p, prob.ld, yd, [tau], [prob.lam_frac * lm], G=G, mu=mu,
+                       eta=eta)
+        S8.iterate(args.burn_in)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        S8.iterate(k)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ms8 = max_over_ranks(ev0.elapsed_time(ev1), dev)
+        u8_line = {"value": whole_job_value(k, ws, ms8), "unit": "iters/s", "ms_per_step": ms8 / k,
+                   "x_stream_gbs": prob.n * prob.p / (ms8 / k / 1000.0) / 1e9, "backend": S8.backend}
+        del S8
 
     # e2e through the public C-ABI host-buffer entry (fsqr_fit_host): H2D copy of X and y from pinned
     # memory, setup, k iterations and the D2H read of beta all inside the timed region.
@@ -273,14 +291,18 @@ def run_ours(args):
         yp = torch.empty(prob.n, dtype=torch.float64, pin_memory=True)
         yp.numpy()[:] = prob.y
         torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         beta_h, _ = fs.fsqr_fit_host(Xp.numpy(), prob.storage, prob.n, prob.p, prob.ld, yp.numpy(), [tau],
-                                     [prob.lam_frac * lm], k, opt=fs.default_options(G=G, mu=mu), eta=eta)
+                                     [prob.lam_frac * lm], k, opt=fs.default_options(G=G, mu=mu), eta=eta,
+                                     flags=flags)
         torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        e2e = {"value": k / dt, "unit": "iters/s", "h2d_bytes_per_step": (prob.X.nbytes + prob.y.nbytes) / k,
+        dt = max_over_ranks((time.perf_counter() - t0) * 1000.0, dev) / 1000.0
+        e2e = {"value": whole_job_value(k, ws, dt * 1000.0), "unit": "iters/s", "h2d_bytes_per_step": (prob.X.nbytes + prob.y.nbytes) / k,
                "d2h_bytes_per_step": beta_h.nbytes / k,
-               "note": "one fsqr_fit_host call: H2D of X,y (pinned) + setup (eta given) + k iterations + D2H beta"}
+               "note": "one fsqr_fit_host call: H2D of X,y (pinned, u8) + setup (eta given"
+                       + (", 2-bit repack" if pack else "") + ") + k iterations + D2H beta"}
         del Xp
 
     # time to KKT tolerance: fsqr_solve from the cold start (beta=0, z=y, theta=0),
@@ -305,12 +327,14 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": ws, "steps": k, "warmup": args.warmup,
             "ms_per_step": total_ms / k, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "u8xs8->s32 exact, f64", "data": "synthetic",
+            "dtype": ("u2" if pack else "u8") + "xs8->s32 exact, f64", "data": "synthetic",
             "config": {"workload": "C5 design/response, single RHS tau=0.5 (BASELINE metric)", "n": prob.n,
-                       "p": prob.p, "storage": "u8", "tau": tau, "lambda": prob.lam_frac * lm, "lambda_frac":
+                       "p": prob.p, "storage": "u8 input" + (", repacked to 2 bits at create (FSQR_DESIGN_PACK2)"
+                                                             if pack else ", streamed as u8"), "tau": tau, "lambda": prob.lam_frac * lm, "lambda_frac":
                        prob.lam_frac, "G": G, "mu": mu, "burn_in": args.burn_in, "support": nnz,
-                       "l2": "X (10 GB) >> L2 (126 MB): no flush needed", "parallelism": f"replicas x{ws}",
+                       "l2": f"X ({xbytes / 1e9:.1f} GB streamed) >> L2 (126 MB): no flush needed", "parallelism": f"replicas x{ws}",
                        "backend": S.backend, "setup_s": t_setup, "datagen_s": t_gen},
+            "u8_storage": u8_line,
             "x_stream_gbs": xbytes / (total_ms / k / 1000.0) / 1e9,
             "x_stream_frac_of_peak": xbytes / (total_ms / k / 1000.0) / 1e9 / peak,
             "stage_ms_per_step": {"k2_xt_theta_prox": stage_ms[0] / k, "k1_forward": stage_ms[1] / k,
@@ -338,6 +362,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="m")
     ap.add_argument("--burn-in", dest="burn_in", type=int, default=200)
+    ap.add_argument("--storage", default="pack2", choices=["u8", "pack2"],
+                    help="device layout of the u8 genotype input: as is, or repacked to 2 bits at create")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-kkt", action="store_true")

@@ -73,12 +73,22 @@ typedef enum {
   FSQR_MCP = 2              /* p'_lambda of E17 (L363-369), a > 1 (a = 3 in the paper's studies, L404) */
 } fsqr_penalty;
 
+/* fsqr_design.flags */
+enum {
+  /* U8 storage only: at create, repack the codes into an OWNED 2-bit copy (fsqr_pack2) and run the
+   * PACKED2 kernels on it, so every iteration streams n*p/4 instead of n*p bytes (DESIGN.md §5,
+   * "storage").  Codes must be in {0..3} (else FSQR_ERR_DATA); data_dev is read only during
+   * create and may be freed afterwards.  Results are those of PACKED2 storage on the same codes. */
+  FSQR_DESIGN_PACK2 = 1
+};
+
 typedef struct {
   int32_t storage;          /* fsqr_storage */
-  int32_t reserved;
+  int32_t flags;            /* FSQR_DESIGN_* bits, 0 = none */
   int64_t n;                /* observations, 2 <= n <= 65536 */
   int64_t p;                /* stored columns (the intercept is virtual and not stored) */
-  const void* data_dev;     /* BORROWED: [p][ld] column-major; must stay alive and unmodified for the ctx lifetime */
+  const void* data_dev;     /* BORROWED: [p][ld] column-major; must stay alive and unmodified for the ctx lifetime
+                               (with FSQR_DESIGN_PACK2: only during fsqr_create) */
   int64_t ld;               /* column stride in elements (F32) or bytes (U8, PACKED2); padding must be zero */
   const double* mean_dev;   /* optional [p] m_j (NULL: computed, a0) */
   const double* scale_dev;  /* optional [p] s_j (NULL: computed, a0); both or neither */
@@ -249,6 +259,17 @@ const char* fsqr_backend_name(const fsqr_ctx* ctx);
 fsqr_status fsqr_fit_host(const fsqr_design* X_host, const double* y_host, int32_t n_rhs, const double* tau_host,
                           const double* lambda_host, const fsqr_options* opt, int64_t iters, double* beta_host,
                           fsqr_result* out, void* stream);
+
+/*
+ * Repack uint8 genotype codes into the PACKED2 layout (north_star subsystem (1): "uint8 or 2-bit
+ * packed {0,1,2}").  x8_dev: [p][ld8] bytes (ld8 >= n, ld8 % 16 == 0, 16-byte aligned); x2_dev:
+ * [p][ld2] bytes (ld2 >= ceil(n/4), ld2 % 16 == 0, 16-byte aligned), caller-owned, fully written
+ * (sample i of column c at bits 2*(i%4) of byte c*ld2 + i/4, padding zero).  Returns
+ * FSQR_ERR_DATA if any code of the first n rows exceeds 3 (x2_dev contents then unspecified),
+ * FSQR_ERR_CONFIG for bad sizes.  Synchronises `stream`.
+ */
+fsqr_status fsqr_pack2(const uint8_t* x8_dev, int64_t ld8, int64_t n, int64_t p, uint8_t* x2_dev, int64_t ld2,
+                       void* stream);
 
 const char* fsqr_last_error(const fsqr_ctx* ctx);
 const char* fsqr_global_error(void);

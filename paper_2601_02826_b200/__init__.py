@@ -34,8 +34,11 @@ class FsqrError(RuntimeError):
         self.status = status
 
 
+DESIGN_PACK2 = 1   # fsqr_design.flags: repack U8 codes to 2-bit at create
+
+
 class fsqr_design(ctypes.Structure):
-    _fields_ = [("storage", ctypes.c_int32), ("reserved", ctypes.c_int32), ("n", ctypes.c_int64),
+    _fields_ = [("storage", ctypes.c_int32), ("flags", ctypes.c_int32), ("n", ctypes.c_int64),
                 ("p", ctypes.c_int64), ("data_dev", ctypes.c_void_p), ("ld", ctypes.c_int64),
                 ("mean_dev", ctypes.c_void_p), ("scale_dev", ctypes.c_void_p)]
 
@@ -57,7 +60,7 @@ EXPORTS = ["fsqr_default_options", "fsqr_create", "fsqr_iterate", "fsqr_solve", 
            "fsqr_get_beta", "fsqr_get_state", "fsqr_set_state", "fsqr_set_lambda", "fsqr_lambda_max",
            "fsqr_get_eta", "fsqr_get_colstats", "fsqr_path", "fsqr_path_beta", "fsqr_trace", "fsqr_iterations",
            "fsqr_profile_iterate", "fsqr_hbic", "fsqr_set_lambda_weights", "fsqr_lla", "fsqr_pivotal", "fsqr_set_lambda2", "fsqr_path_hbic",
-           "fsqr_backend_name", "fsqr_fit_host", "fsqr_last_error", "fsqr_global_error", "fsqr_status_str",
+           "fsqr_backend_name", "fsqr_fit_host", "fsqr_pack2", "fsqr_last_error", "fsqr_global_error", "fsqr_status_str",
            "fsqr_destroy"]
 
 
@@ -113,6 +116,7 @@ def load(build_if_missing: bool = True):
     L.fsqr_backend_name.restype = ctypes.c_char_p
     L.fsqr_fit_host.argtypes = [ctypes.POINTER(fsqr_design), P, I32, P, P, ctypes.POINTER(fsqr_options), I64, P,
                                 ctypes.POINTER(fsqr_result), P]
+    L.fsqr_pack2.argtypes = [P, I64, I64, I64, P, I64, P]
     L.fsqr_last_error.argtypes = [ctxp]
     L.fsqr_last_error.restype = ctypes.c_char_p
     L.fsqr_global_error.argtypes = []
@@ -124,7 +128,7 @@ def load(build_if_missing: bool = True):
     for name in ("fsqr_create", "fsqr_iterate", "fsqr_solve", "fsqr_objective", "fsqr_kkt", "fsqr_get_beta",
                  "fsqr_get_state", "fsqr_set_state", "fsqr_set_lambda", "fsqr_lambda_max", "fsqr_get_eta",
                  "fsqr_get_colstats", "fsqr_path", "fsqr_path_beta", "fsqr_trace", "fsqr_fit_host", "fsqr_hbic",
-                 "fsqr_set_lambda_weights", "fsqr_lla", "fsqr_pivotal", "fsqr_set_lambda2", "fsqr_path_hbic"):
+                 "fsqr_set_lambda_weights", "fsqr_lla", "fsqr_pivotal", "fsqr_set_lambda2", "fsqr_path_hbic", "fsqr_pack2"):
         getattr(L, name).restype = S
     _lib = L
     return L
@@ -167,10 +171,10 @@ def default_options(**kw) -> fsqr_options:
 # ------------------------------------------------------------------ C-ABI mirrors
 
 def fsqr_create(X, storage: int, n: int, p: int, ld: int, y, taus, lambdas, lambda_w=None, opt=None, stream=None,
-                eta=None, mean=None, scale=None):
+                eta=None, mean=None, scale=None, flags: int = 0):
     """X, y, lambda_w, mean, scale: CUDA tensors (borrowed X); taus, lambdas: sequences; returns ctx handle."""
     L = load()
-    d = fsqr_design(storage, 0, n, p, _ptr(X).value, ld, _ptr(mean).value if mean is not None else None,
+    d = fsqr_design(storage, flags, n, p, _ptr(X).value, ld, _ptr(mean).value if mean is not None else None,
                     _ptr(scale).value if scale is not None else None)
     taus = np.ascontiguousarray(taus, dtype=np.float64)
     lambdas = np.ascontiguousarray(lambdas, dtype=np.float64)
@@ -342,10 +346,10 @@ def fsqr_backend_name(ctx) -> str:
 
 
 def fsqr_fit_host(X: np.ndarray, storage: int, n: int, p: int, ld: int, y: np.ndarray, taus, lambdas, iters: int,
-                  opt=None, stream=None, eta=None) -> tuple:
+                  opt=None, stream=None, eta=None, flags: int = 0) -> tuple:
     """End-to-end call with HOST buffers (X should be pinned for speed); returns (beta [R, p+1], result dict)."""
     L = load()
-    d = fsqr_design(storage, 0, n, p, _ptr(X).value, ld, None, None)
+    d = fsqr_design(storage, flags, n, p, _ptr(X).value, ld, None, None)
     taus = np.ascontiguousarray(taus, dtype=np.float64)
     lambdas = np.ascontiguousarray(lambdas, dtype=np.float64)
     yy = np.ascontiguousarray(y, dtype=np.float64)
@@ -362,6 +366,21 @@ def fsqr_fit_host(X: np.ndarray, storage: int, n: int, p: int, ld: int, y: np.nd
     return beta, dict(status=st, iterations=r.iterations)
 
 
+def fsqr_pack2(X8, ld8: int, n: int, p: int, X2=None, stream=None):
+    """Repack u8 codes (CUDA tensor [p, ld8]) into PACKED2 layout; returns (X2 [p, ld2] uint8 tensor, ld2)."""
+    import torch
+
+    ld2 = leading_dim_packed2(n)
+    if X2 is None:
+        X2 = torch.empty((p, ld2), dtype=torch.uint8, device=X8.device)
+    _check(load().fsqr_pack2(_ptr(X8), int(ld8), int(n), int(p), _ptr(X2), int(ld2), _stream(stream)))
+    return X2, ld2
+
+
+def leading_dim_packed2(n: int) -> int:
+    return (((n + 3) // 4 + 15) // 16) * 16
+
+
 def fsqr_destroy(ctx):
     load().fsqr_destroy(ctx)
 
@@ -371,7 +390,7 @@ class Solver:
 
     def __init__(self, X, storage: int, n: int, p: int, ld: int, y, taus, lambdas, G: int = 5, mu: float = 0.0,
                  tol: float = 1e-6, max_iter: int = 100000, backend: int = BACKEND_AUTO, eta=None, lambda_w=None,
-                 max_iter_point: int = 10000, stream=None, **kw):
+                 max_iter_point: int = 10000, stream=None, flags: int = 0, **kw):
         import torch
 
         self.X = X
@@ -381,7 +400,8 @@ class Solver:
         self.taus = list(taus)
         opt = default_options(G=G, mu=mu, tol=tol, max_iter=max_iter, backend=backend,
                               max_iter_point=max_iter_point, **kw)
-        self.ctx = fsqr_create(X, storage, n, p, ld, self.y, taus, lambdas, lambda_w, opt, stream, eta=eta)
+        self.ctx = fsqr_create(X, storage, n, p, ld, self.y, taus, lambdas, lambda_w, opt, stream, eta=eta,
+                               flags=flags)
 
     def __del__(self):
         ctx = getattr(self, "ctx", None)

@@ -416,6 +416,29 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
   if (X->ld < minld || X->ld % align) return set_err(ctx, FSQR_ERR_CONFIG, "ld=%lld invalid (min %lld, multiple of %d)",
                                                      (long long)X->ld, (long long)minld, align);
   if (((uintptr_t)X->data_dev) % 16) return set_err(ctx, FSQR_ERR_CONFIG, "data_dev must be 16-byte aligned");
+  if (X->flags & ~FSQR_DESIGN_PACK2) return set_err(ctx, FSQR_ERR_CONFIG, "unknown design flags 0x%x", X->flags);
+  fsqr_design Xpk;
+  if (X->flags & FSQR_DESIGN_PACK2) {
+    // owned 2-bit copy of the u8 codes; everything below sees PACKED2 storage
+    if (X->storage != FSQR_U8) return set_err(ctx, FSQR_ERR_CONFIG, "FSQR_DESIGN_PACK2 needs U8 storage");
+    const int64_t ld2 = (((X->n + 3) / 4 + 15) / 16) * 16;
+    uint8_t* x2;
+    int* bad2;
+    AL(x2, ld2 * X->p);
+    AL(bad2, 1);
+    launch_pack2((const uint8_t*)X->data_dev, X->ld, (int)X->n, X->p, x2, ld2, bad2, st);
+    CK(cudaGetLastError());
+    int h_bad = 0;
+    CK(cudaMemcpyAsync(&h_bad, bad2, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h_bad) return set_err(ctx, FSQR_ERR_DATA, "FSQR_DESIGN_PACK2: a genotype code exceeds 3");
+    Xpk = *X;
+    Xpk.storage = FSQR_PACKED2;
+    Xpk.flags = 0;
+    Xpk.data_dev = x2;
+    Xpk.ld = ld2;
+    X = &Xpk;
+  }
   fsqr_options o;
   if (opt) o = *opt; else fsqr_default_options(&o);
   if (o.mu == 0.0) o.mu = 2.0 / (double)X->n;   // DESIGN.md reading R2
@@ -1185,6 +1208,29 @@ int64_t fsqr_iterations(fsqr_ctx* ctx) {
   return it;
 }
 
+fsqr_status fsqr_pack2(const uint8_t* x8, int64_t ld8, int64_t n, int64_t p, uint8_t* x2, int64_t ld2, void* stream) {
+  fsqr_ctx* ctx = nullptr;
+  if (!x8 || !x2) return set_err(nullptr, FSQR_ERR_CONFIG, "null argument");
+  if (n < 1 || n > 65536 || p < 1 || ld8 < n || ld8 % 16 || ld2 < (n + 3) / 4 || ld2 % 16 ||
+      ((uintptr_t)x8) % 16 || ((uintptr_t)x2) % 16)
+    return set_err(nullptr, FSQR_ERR_CONFIG, "fsqr_pack2: bad sizes or alignment");
+  cudaStream_t st = (cudaStream_t)stream;
+  int* bad = nullptr;
+  CK(cudaMallocAsync((void**)&bad, sizeof(int), st));
+  cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(int), st);
+  if (e == cudaSuccess) {
+    launch_pack2(x8, ld8, (int)n, p, x2, ld2, bad, st);
+    e = cudaGetLastError();
+  }
+  int h_bad = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(bad, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  CK(e);
+  if (h_bad) return set_err(nullptr, FSQR_ERR_DATA, "fsqr_pack2: a genotype code exceeds 3");
+  return FSQR_OK;
+}
+
 fsqr_status fsqr_fit_host(const fsqr_design* Xh, const double* y_host, int32_t n_rhs, const double* tau_host,
                           const double* lambda_host, const fsqr_options* opt, int64_t iters, double* beta_host,
                           fsqr_result* out, void* stream) {
@@ -1213,6 +1259,10 @@ fsqr_status fsqr_fit_host(const fsqr_design* Xh, const double* y_host, int32_t n
   Xd.mean_dev = nullptr;
   Xd.scale_dev = nullptr;
   fsqr_status s = fsqr_create(&Xd, dy, n_rhs, tau_host, lambda_host, nullptr, opt, stream, &ctx);
+  if (s == FSQR_OK && (Xh->flags & FSQR_DESIGN_PACK2)) {   // the ctx owns its packed copy
+    cudaFreeAsync(dX, st);
+    dX = nullptr;
+  }
   if (s == FSQR_OK) {
     if (iters >= 0) {
       s = fsqr_iterate(ctx, iters, stream);
@@ -1226,7 +1276,7 @@ fsqr_status fsqr_fit_host(const fsqr_design* Xh, const double* y_host, int32_t n
     }
     fsqr_destroy(ctx);
   }
-  cudaFreeAsync(dX, st);
+  if (dX) cudaFreeAsync(dX, st);
   cudaFreeAsync(dy, st);
   cudaStreamSynchronize(st);
   return s;

@@ -374,6 +374,43 @@ __global__ void __launch_bounds__(FT) k_init_state(const Dev D) {
 
 // ---------------------------------------------------------------- setup kernels
 
+// u8 -> PACKED2 repack (fsqr_pack2): one thread per packed 32-bit word = 16 samples of one column.
+// Byte b of the word holds samples 16j+4b..16j+4b+3 at bits 2(i%4): for a little-endian word
+// a = x0|x1<<8|x2<<16|x3<<24 with every x <= 3, (a | a>>6 | a>>12 | a>>18) & 0xFF.
+__global__ void k_pack2(const uint8_t* __restrict__ x8, int64_t ld8, int n, int64_t p, uint32_t* __restrict__ x2,
+                        int64_t ld2, int* bad) {
+  const int64_t wpc = ld2 / 4;   // packed words per column
+  const int64_t total = p * wpc;
+  int flag = 0;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = w / wpc;
+    const int i0 = (int)(w - c * wpc) * 16;
+    uint32_t a[4];
+    const uint8_t* src = x8 + c * ld8 + i0;
+    if (i0 + 16 <= n) {
+      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(src));
+      a[0] = v.x, a[1] = v.y, a[2] = v.z, a[3] = v.w;
+    } else {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        uint32_t u = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (i0 + 4 * b + e < n) u |= (uint32_t)src[4 * b + e] << (8 * e);
+        a[b] = u;
+      }
+    }
+    uint32_t out = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      flag |= (a[b] & 0xFCFCFCFCu) != 0;
+      out |= ((a[b] | (a[b] >> 6) | (a[b] >> 12) | (a[b] >> 18)) & 0xFFu) << (8 * b);
+    }
+    x2[w] = out;
+  }
+  if (__syncthreads_or(flag) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
 template <int ST>
 __global__ void k_colstats_int(const Dev D, int32_t* colsum, double* mean, double* inv_sd, double* sd, int* bad) {
   const int lane = threadIdx.x & 31;
@@ -793,6 +830,10 @@ void launch_finalize(const Dev& D, cudaStream_t st) {
     launch_pdl(k_finalize, dim3(1), dim3(FT), 0, st, D);
   else
     launch_pdl(k_finalize_mc, dim3((D.n + FIN_THREADS - 1) / FIN_THREADS, D.R), dim3(FIN_THREADS), 0, st, D);
+}
+void launch_pack2(const uint8_t* x8, int64_t ld8, int n, int64_t p, uint8_t* x2, int64_t ld2, int* bad,
+                  cudaStream_t st) {
+  k_pack2<<<148 * 8, 256, 0, st>>>(x8, ld8, n, p, reinterpret_cast<uint32_t*>(x2), ld2, bad);
 }
 void launch_init_state(const Dev& D, cudaStream_t st) { k_init_state<<<1, FT, 0, st>>>(D); }
 void launch_colstats(const Dev& D, int32_t* colsum, double* mean, double* inv_sd, double* sd, int* bad,

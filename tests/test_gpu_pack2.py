@@ -1,0 +1,107 @@
+"""GPU tests of the u8 -> 2-bit repack (fsqr_pack2 and the FSQR_DESIGN_PACK2 create flag,
+include/fsqr.h; north_star storage subsystem (1), "uint8 or 2-bit packed {0,1,2}").
+
+The expected bytes come from the seeded generator's own PACKED2 output for the same codes
+(datagen writes both layouts from one draw), never from the device path; the solver equalities
+are exact because the PACKED2 kernels compute exact integer products on identical codes."""
+import numpy as np
+import pytest
+
+import datagen
+from gpu_helpers import rel, to_device
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("n,p", [(999, 300), (1024, 129), (17, 5), (2, 3), (4097, 64)])
+def test_pack2_matches_generator_layout(cuda_ok, n, p):
+    import torch
+
+    import paper_2601_02826_b200 as fs
+
+    a = datagen.make("c2", n=n, p=p, storage=fs.U8)
+    b = datagen.make("c2", n=n, p=p, storage=fs.PACKED2)
+    X8 = torch.from_numpy(a.X).cuda()
+    X2 = torch.full((p, b.ld), 0xAB, dtype=torch.uint8, device="cuda")   # garbage: every byte must be written
+    out, ld2 = fs.fsqr_pack2(X8, a.ld, n, p, X2)
+    assert ld2 == b.ld
+    np.testing.assert_array_equal(out.cpu().numpy(), b.X)
+
+
+def test_pack2_rejects_codes_above_3(cuda_ok):
+    import torch
+
+    import paper_2601_02826_b200 as fs
+
+    a = datagen.make("c2", n=300, p=40, storage=fs.U8)
+    X = a.X.copy()
+    X[37, 211] = 4
+    with pytest.raises(fs.FsqrError, match="ERR_DATA"):
+        fs.fsqr_pack2(torch.from_numpy(X).cuda(), a.ld, a.n, a.p)
+    y = torch.from_numpy(a.y).cuda()
+    with pytest.raises(fs.FsqrError, match="ERR_DATA"):
+        fs.Solver(torch.from_numpy(X).cuda(), fs.U8, a.n, a.p, a.ld, y, [0.5], [0.01], flags=fs.DESIGN_PACK2)
+    # code 3 is representable and accepted
+    X[37, 211] = 3
+    fs.fsqr_pack2(torch.from_numpy(X).cuda(), a.ld, a.n, a.p)
+
+
+def test_pack2_flag_needs_u8(cuda_ok):
+    import torch
+
+    import paper_2601_02826_b200 as fs
+
+    b = datagen.make("c2", n=300, p=40, storage=fs.PACKED2)
+    X, y = to_device(b)
+    with pytest.raises(fs.FsqrError, match="ERR_CONFIG"):
+        fs.Solver(X, fs.PACKED2, b.n, b.p, b.ld, y, [0.5], [0.01], flags=fs.DESIGN_PACK2)
+    with pytest.raises(fs.FsqrError, match="ERR_CONFIG"):
+        fs.Solver(X, fs.PACKED2, b.n, b.p, b.ld, y, [0.5], [0.01], flags=4)
+    del torch
+
+
+@pytest.mark.parametrize("name,taus", [("c2", [0.5]), ("c5", [0.1, 0.5, 0.9]), ("c5", [0.1 * k for k in range(1, 10)])])
+def test_create_pack2_equals_packed_storage(cuda_ok, name, taus):
+    """A solver created from u8 codes with FSQR_DESIGN_PACK2 is the PACKED2 solver: bit-identical
+    state after the same iterations, and it no longer reads the u8 buffer (freed and overwritten)."""
+    import torch
+
+    import paper_2601_02826_b200 as fs
+
+    a = datagen.make(name, n=1500, p=2600, storage=fs.U8)
+    b = datagen.make(name, n=1500, p=2600, storage=fs.PACKED2)
+    eta = [40.0] * 5
+    lams = [0.03] * len(taus)
+    X8, y = to_device(a)
+    SA = fs.Solver(X8, fs.U8, a.n, a.p, a.ld, y, taus, lams, G=5, eta=eta, flags=fs.DESIGN_PACK2)
+    X8.fill_(0xFF)          # the ctx must hold its own copy
+    del X8
+    torch.cuda.empty_cache()
+    X2, _ = to_device(b)
+    SB = fs.Solver(X2, fs.PACKED2, b.n, b.p, b.ld, y, taus, lams, G=5, eta=eta)
+    assert SA.backend == SB.backend == "tc"
+    SA.iterate(70)
+    SB.iterate(70)
+    for u, v in zip(SA.state(), SB.state()):
+        np.testing.assert_array_equal(u, v)
+    np.testing.assert_array_equal(SA.objective(), SB.objective())
+    np.testing.assert_array_equal(SA.beta(1), SB.beta(1))
+    # and it is the u8 solver: the products are exact integers on the same codes
+    X8, _ = to_device(a)
+    SC = fs.Solver(X8, fs.U8, a.n, a.p, a.ld, y, taus, lams, G=5, eta=eta)
+    SC.iterate(70)
+    for u, v in zip(SA.state(), SC.state()):
+        assert rel(u, v) < 1e-12
+
+
+def test_fit_host_pack2(cuda_ok):
+    import paper_2601_02826_b200 as fs
+
+    a = datagen.make("c2", n=700, p=1900, storage=fs.U8)
+    b = datagen.make("c2", n=700, p=1900, storage=fs.PACKED2)
+    eta = [25.0] * 5
+    ba, _ = fs.fsqr_fit_host(a.X, fs.U8, a.n, a.p, a.ld, a.y, [0.5], [0.04], 80, opt=fs.default_options(G=5),
+                             eta=eta, flags=fs.DESIGN_PACK2)
+    bb, _ = fs.fsqr_fit_host(b.X, fs.PACKED2, b.n, b.p, b.ld, b.y, [0.5], [0.04], 80, opt=fs.default_options(G=5),
+                             eta=eta)
+    np.testing.assert_array_equal(ba, bb)
