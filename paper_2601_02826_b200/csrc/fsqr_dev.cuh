@@ -31,7 +31,7 @@ enum { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_NUMERIC = 3 };
 struct Dev {
   // sizes / layout
   int n, R, G, storage, npad, ldk;
-  int k1_tc;                        // forward product: 0 k1_bulk (CUDA cores), 1 k1_tc (TMEM transpose), 2 k1_tcg (gather4)
+  int k1_tc;                        // forward product: 0 k1_bulk (CUDA cores), 1 k1_tc (TMEM transpose), 2 k1_tcg (gather4), 3 k1_tcp (2-bit, smem unpack)
   const void* tmG;                  // host pointer to the gather4 tensor map (launcher side only)
   int x_policy;                     // L2 hint of the X stream in K2: 0 evict_first, 1 normal, 2 evict_last
   int k1_policy;                    // L2 hint of the forward gather: 0 evict_first, 1 normal, 2 evict_last
@@ -62,6 +62,7 @@ struct Dev {
   // support lists, double-buffered by iteration parity
   int32_t* sup_idx[2];              // data column index
   double* sup_c[2];                 // [cap*R] beta_j / s_j
+  int32_t* sup_cs[2];               // colsum_j of each entry (forward-product centring term)
   double* sup_b[2];                 // [cap*R] beta_j
   int* sup_cnt;                     // [2]
   unsigned long long* cmax;         // [2][R] bits of max |beta_j/s_j|
@@ -323,6 +324,8 @@ struct K2Ctx {
   const double* beta_in;
   double* beta_out;
   int32_t* sidx;
+  int32_t* scs;
+  const int32_t* colsum;
   double* sc;
   double* sb;
   int* scnt;
@@ -430,6 +433,7 @@ __device__ __forceinline__ void support_append(const K2Ctx<RMAX>& C, bool nz, in
   if (nz) {
     const int e = base + __popc(m & ((1u << lane) - 1u));
     C.sidx[e] = (int32_t)c;
+    C.scs[e] = C.colsum[c];
 #pragma unroll
     for (int r = 0; r < RMAX; ++r) {
       if (r < C.R) {
@@ -488,4 +492,6 @@ cudaError_t k1_tc_init();
 cudaError_t k1_tcg_init();
 void launch_k1_tcg(const Dev& D, const void* tmG, int grid, cudaStream_t st, int cur);
 void launch_k1_tc(const Dev& D, int grid, cudaStream_t st, int cur);
+void launch_k1_tcp(const Dev& D, int grid, cudaStream_t st, int cur);
+cudaError_t k1_tcp_init();
 int k2_tc_supported(int npad);

@@ -428,6 +428,10 @@ void launch_k1_mode(const Dev& D, int grid, cudaStream_t st, int cur) {
     launch_k1_tcg(D, D.tmG, grid, st, cur);
     return;
   }
+  if (D.k1_tc == 3 && D.storage == 2) {
+    launch_k1_tcp(D, grid, st, cur);
+    return;
+  }
   if (D.k1_tc == 1 && D.storage != 0) {
     launch_k1_tc(D, grid, st, cur);
     return;

@@ -12,6 +12,8 @@ __device__ void k2_load_ctx(const Dev& D, K2Ctx<RMAX>& C) {
   C.beta_in = D.beta[par];
   C.beta_out = D.beta[par ^ 1];
   C.sidx = D.sup_idx[par ^ 1];
+  C.scs = D.sup_cs[par ^ 1];
+  C.colsum = D.colsum;
   C.sc = D.sup_c[par ^ 1];
   C.sb = D.sup_b[par ^ 1];
   C.scnt = D.sup_cnt + (par ^ 1);

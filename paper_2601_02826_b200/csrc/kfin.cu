@@ -734,6 +734,7 @@ __global__ void k_build_support(const Dev D, int par) {
     if (nz) {
       const int e = base + __popc(m & ((1u << lane) - 1u));
       D.sup_idx[par][e] = (int32_t)c;
+      D.sup_cs[par][e] = D.colsum[c];
       for (int r = 0; r < R; ++r) {
         const double b = beta[(c + 1) * R + r];
         const double cv = b * D.inv_sd[c];

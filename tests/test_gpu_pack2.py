@@ -105,3 +105,27 @@ def test_fit_host_pack2(cuda_ok):
     bb, _ = fs.fsqr_fit_host(b.X, fs.PACKED2, b.n, b.p, b.ld, b.y, [0.5], [0.04], 80, opt=fs.default_options(G=5),
                              eta=eta)
     np.testing.assert_array_equal(ba, bb)
+
+
+@pytest.mark.parametrize("n,p,taus", [(1500, 2600, [0.5]), (999, 3100, [0.3, 0.7]), (4097, 1800, [0.2, 0.5, 0.8]),
+                                      (2500, 2000, [0.1 * k for k in range(1, 10)]),
+                                      (700, 1500, [k / 17 for k in range(1, 17)])])
+def test_k1_tcp_equals_cuda_core_forward(cuda_ok, monkeypatch, n, p, taus):
+    """The tensor-core forward product for 2-bit storage (k1_tcp: on-chip unpack into the
+    swizzled A tile) forms the same exact fixed-point sums as the CUDA-core k1_bulk: the whole
+    state after k iterations is bit-identical (several row tiles, ragged last slab, 1-16 RHS)."""
+    import paper_2601_02826_b200 as fs
+
+    b = datagen.make("c5", n=n, p=p, storage=fs.PACKED2)
+    X, y = to_device(b)
+    eta = [40.0] * 5
+    lams = [0.02] * len(taus)
+    out = []
+    for mode in ("bulk", "tcp"):
+        monkeypatch.setenv("FSQR_K1", mode)
+        S = fs.Solver(X, fs.PACKED2, b.n, b.p, b.ld, y, taus, lams, G=5, eta=eta)
+        S.iterate(60)
+        out.append(S.state() + (S.objective(),))
+        del S
+    for u, v in zip(out[0], out[1]):
+        np.testing.assert_array_equal(u, v)
