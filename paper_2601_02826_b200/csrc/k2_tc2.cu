@@ -27,27 +27,35 @@
 
 #include "k2_common.cuh"
 
+#ifndef K2TC2_CW
+#define K2TC2_CW 8   // converter warps (two per SM sub-partition: the unpack loop is latency-bound with one)
+#endif
+
 namespace {
 
 constexpr int TILE_M = 128;               // columns per tile (UMMA M)
 constexpr int PK = 128;                   // packed bytes per column per stage
 constexpr int KS = 4 * PK;                // samples (K) per stage
 constexpr int A_BYTES = TILE_M * PK;      // 16 KB packed A per stage
-constexpr int NAB = 3;                    // TMEM A buffers
 constexpr int A_COLS = KS / 4;            // TMEM columns per A buffer (4 int8 per 32-bit cell)
-constexpr int A_COL0 = 128;               // A buffers start after the accumulators (2*NPAD <= 128)
 
 // warps: 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4..4+CW-1 convert, then 4 epilogue warps.  One RHS
 // (the C4 workload) keeps few registers per thread, so it affords 8 converter warps (two per SM
 // sub-partition: the unpack loop is latency-bound with one); more RHS keep 4.
 template <int NPAD, int RM>
 struct Cfg2 {
-  static constexpr int CW = RM == 1 ? 8 : 4;
+  static constexpr int CW = K2TC2_CW;
   // NPAD == 16: one accumulator per code plane q, so the converter can leave the codes in place
   // ((w & (3 << 2q)) = x * 4^q, one LOP per word instead of shift + mask); the epilogue divides
-  // each plane's exact sum by 4^q.  Needs 2 x 4 x 16 = 128 TMEM columns (fits before A_COL0).
+  // each plane's exact sum by 4^q.  Needs 2 x 4 x 16 = 128 TMEM columns.
+  // NPAD > 16 (several RHS): four planes would not fit next to the A buffers, so two scale
+  // groups: with w4 = w >> 4 (one SHF per word), planes 0 and 2 are w & M and w4 & M (x 1),
+  // planes 1 and 3 are w & (M << 2) and w4 & (M << 2) (x 4): 5 instructions per word instead of 8.
   static constexpr bool SPLITQ = NPAD == 16;
-  static constexpr int ACC_COLS = SPLITQ ? 4 * NPAD : NPAD;   // columns of one accumulator buffer
+  static constexpr int ACC_COLS = SPLITQ ? 4 * NPAD : 2 * NPAD;   // columns of one accumulator buffer
+  static constexpr int A_COL0 = 2 * ACC_COLS;                     // A buffers after the two accumulators
+  static constexpr int NAB = (512 - A_COL0) / A_COLS < 3 ? (512 - A_COL0) / A_COLS : 3;   // TMEM A buffers
+  static_assert(NAB >= 2, "TMEM budget");
   static constexpr int THREADS = 32 * (8 + CW);
   static constexpr int B_ATOM = NPAD * 128;
   static constexpr int B_BYTES = 4 * B_ATOM;
@@ -104,6 +112,7 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
   uint64_t* full = (uint64_t*)(smem + CF::STAGES * CF::STAGE);
   uint64_t* empty = full + CF::STAGES;
   uint64_t* afull = empty + CF::STAGES;
+  constexpr int NAB = CF::NAB, A_COL0 = CF::A_COL0;
   uint64_t* aempty = afull + NAB;
   uint64_t* tfull = aempty + NAB;
   uint64_t* tempty = tfull + 2;
@@ -200,7 +209,7 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
   } else if (wid == 1) {
     // ===== MMA issuer: the whole warp walks the pipeline, one elected lane issues =====
     {
-      constexpr uint32_t idesc = CF::SPLITQ ? idesc_u8s8(NPAD) : idesc_i8(NPAD);
+      constexpr uint32_t idesc = CF::SPLITQ ? idesc_u8s8(NPAD) : idesc_i8(NPAD);   // (codes x 4 <= 12 fit s8)
       const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
       const uint32_t sB0 = smem_u32(sB);
       int stage = 0, ab = 0;
@@ -221,8 +230,9 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < KS / 32; ++kk) {   // K = 32 samples per kind::i8 MMA; plane q = kk / 4
-              const uint32_t dq = CF::SPLITQ ? d_tmem + (uint32_t)((kk >> 2) * NPAD) : d_tmem;
-              const bool accum = CF::SPLITQ ? (kb != 0 || (kk & 3) != 0) : (kb | kk) != 0;
+              const uint32_t dq = CF::SPLITQ ? d_tmem + (uint32_t)((kk >> 2) * NPAD)
+                                             : d_tmem + (uint32_t)(((kk >> 2) & 1) * NPAD);
+              const bool accum = CF::SPLITQ ? (kb != 0 || (kk & 3) != 0) : (kb != 0 || (kk & 11) != 0);   // first of each group: kk = 0, 4
               umma_i8_tmem_a(dq, a_tmem + (uint32_t)(8 * kk),
                              bdesc0 + (uint64_t)((kk >> 2) * (CF::B_ATOM >> 4) + 2 * (kk & 3)), idesc, accum);
             }
@@ -259,7 +269,7 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
         mbar_wait(&full[stage], phase);
         mbar_wait(&aempty[ab], aphase ^ 1);
         tc_fence_after();
-        uint32_t w[NW];
+        uint32_t w[NW], w4[CF::SPLITQ ? 1 : NW];
         const uint8_t* row = sA + stage * A_BYTES + c * PK;
 #pragma unroll
         for (int jj = 0; jj < CH; ++jj) {   // logical 16-byte chunk j sits at chunk j ^ (c & 7) (SWIZZLE_128B)
@@ -271,12 +281,17 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
           w[4 * jj + 3] = v.w;
         }
         const uint32_t abase = tmem_base + lane_off + (uint32_t)(A_COL0 + ab * A_COLS + h * NW);
+        if constexpr (!CF::SPLITQ) {
+#pragma unroll
+          for (int u = 0; u < NW; ++u) w4[u] = w[u] >> 4;
+        }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           uint32_t o[NW];
 #pragma unroll
           for (int u = 0; u < NW; ++u)
-            o[u] = CF::SPLITQ ? (w[u] & (0x03030303u << (2 * q))) : ((w[u] >> (2 * q)) & 0x03030303u);
+            o[u] = CF::SPLITQ ? (w[u] & (0x03030303u << (2 * q)))
+                              : ((q & 2 ? w4[u] : w[u]) & (0x03030303u << (2 * (q & 1))));
           if constexpr (NW == 32) tmem_st32(abase + (uint32_t)(32 * q), o);
           else tmem_st16(abase + (uint32_t)(32 * q), o);
         }
@@ -315,14 +330,15 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
 #pragma unroll
           for (int u = 0; u < 16; ++u) dv[u] += ((int32_t)v[u]) >> (2 * pq);
         }
-      } else {
+      } else {   // scale group 0 (planes 0, 2) + scale group 1 (planes 1, 3) / 4, exactly
 #pragma unroll
         for (int h = 0; h < NPAD / 16; ++h) {
-          uint32_t v[16];
-          tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NPAD + h * 16), v);
+          uint32_t v[16], v1[16];
+          tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * CF::ACC_COLS + h * 16), v);
+          tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * CF::ACC_COLS + NPAD + h * 16), v1);
           tmem_wait_ld();
 #pragma unroll
-          for (int u = 0; u < 16; ++u) dv[h * 16 + u] = (int32_t)v[u];
+          for (int u = 0; u < 16; ++u) dv[h * 16 + u] = (int32_t)v[u] + ((int32_t)v1[u] >> 2);
         }
       }
       tc_fence_before();

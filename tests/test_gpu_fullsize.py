@@ -147,9 +147,11 @@ def test_c2_full_three_taus_trajectory(cuda_ok):
         assert obj[r] == pytest.approx(oracle.objective(d, prob.y, tau, lv, o["beta"]), rel=1e-4)
 
 
-def test_m_full_trajectory(cuda_ok):
+@pytest.mark.parametrize("pack", [False, True])
+def test_m_full_trajectory(cuda_ok, pack):
     """The bench workload M (n=10k, p=1M, u8, G=48) at full size: 6 iterations from the cold
-    start (the last one through bench.py's launch path), every element compared."""
+    start (the last one through bench.py's launch path), every element compared; streamed as
+    u8, and repacked to 2 bits at create (FSQR_DESIGN_PACK2, bench.py's default layout)."""
     import paper_2601_02826_b200 as fs
 
     prob = datagen.make("m")
@@ -159,7 +161,8 @@ def test_m_full_trajectory(cuda_ok):
     lm, _ = oracle.lambda_max(d, prob.y, tau)
     lam = prob.lam_frac * lm
     X, y = to_device(prob)
-    S = fs.Solver(X, prob.storage, prob.n, prob.p, prob.ld, y, [tau], [lam], G=G, mu=mu, eta=eta)
+    S = fs.Solver(X, prob.storage, prob.n, prob.p, prob.ld, y, [tau], [lam], G=G, mu=mu, eta=eta,
+                  flags=fs.DESIGN_PACK2 if pack else 0)
     assert S.backend == "tc"
     np.testing.assert_allclose(S.lambda_max()[0], lm, rtol=1e-10)
     k = 6
@@ -178,15 +181,17 @@ def test_m_full_trajectory(cuda_ok):
 
 # ------------------------------------------------------------------ one-step properties at full size
 
-@pytest.mark.parametrize("name", ["m", "c3", "c4", "c5"])
+@pytest.mark.parametrize("name", ["m", "m_pack2", "c3", "c4", "c5"])
 def test_full_size_step_properties(cuda_ok, name):
     import paper_2601_02826_b200 as fs
 
+    flags = fs.DESIGN_PACK2 if name.endswith("_pack2") else 0
+    name = name.replace("_pack2", "")
     prob = datagen.make(name)
     X, y = to_device(prob)
     mu, G = 2.0 / prob.n, prob.G
     taus = list(prob.taus)
-    S = fs.Solver(X, prob.storage, prob.n, prob.p, prob.ld, y, taus, [1.0] * len(taus), G=G, mu=mu)
+    S = fs.Solver(X, prob.storage, prob.n, prob.p, prob.ld, y, taus, [1.0] * len(taus), G=G, mu=mu, flags=flags)
     lm = S.lambda_max()
     frac = prob.lam_frac if prob.path_points == 1 else 0.1   # C5: a mid-path point (0.1 lambda_max)
     lams = [frac * v for v in lm]

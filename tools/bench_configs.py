@@ -50,16 +50,19 @@ def run(name, args):
     X = torch.from_numpy(prob.X).cuda()
     y = torch.from_numpy(prob.y).cuda()
     mu = 2.0 / prob.n
-    xbytes = prob.X.nbytes
+    pack = args.pack2 and prob.storage == datagen.STORAGE_U8
+    xbytes = prob.n * prob.p // 4 if pack else prob.X.nbytes   # bytes each K2 pass streams
     taus = prob.taus
-    base = dict(config=name, n=prob.n, p=prob.p, storage=datagen.STORAGE_NAMES[prob.storage], G=prob.G,
+    base = dict(config=name, n=prob.n, p=prob.p,
+                storage=datagen.STORAGE_NAMES[prob.storage] + (" -> 2-bit (FSQR_DESIGN_PACK2)" if pack else ""), G=prob.G,
                 x_bytes=xbytes, datagen_s=t_gen)
     groups = [taus] if (name == "c5" or len(taus) == 1) else [[t] for t in taus] + [taus]
     for tg in groups:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         S = fs.Solver(X, prob.storage, prob.n, prob.p, prob.ld, y, tg, [1.0] * len(tg), G=prob.G, mu=mu,
-                      tol=args.tol, max_iter=args.max_iter, backend=args.backend)
+                      tol=args.tol, max_iter=args.max_iter, backend=args.backend,
+                      flags=fs.DESIGN_PACK2 if pack else 0)
         lm = S.lambda_max()
         setup_s = time.perf_counter() - t0
         rec = dict(base, taus=tg, backend=S.backend, setup_s=setup_s, lambda_max=lm.tolist())
@@ -75,6 +78,8 @@ def run(name, args):
                        k2_frac_of_peak=xbytes / (st[0] / args.steps / 1e3) / 1e9 / peak(),
                        support=int(S.trace(1)[-1, :, 4].max()))
             emit(rec, args.out)
+            if args.no_kkt:
+                continue
             # the full warm-started path from the cold start
             S.set_state(np.zeros((len(tg), prob.p + 1)), np.tile(prob.y, (len(tg), 1)),
                         np.zeros((len(tg), prob.n)))
@@ -107,7 +112,7 @@ def run(name, args):
                    k2_frac_of_peak=xbytes / (st[0] / args.steps / 1e3) / 1e9 / peak(),
                    support=int(S.trace(1)[-1, :, 4].max()))
         emit(rec, args.out)
-        if args.pivotal and prob.storage == datagen.STORAGE_U8 and len(tg) == 1:
+        if args.pivotal and prob.storage == datagen.STORAGE_U8 and not pack and len(tg) == 1:
             S.pivotal(128, seed=1)          # first call allocates and builds its tensor maps
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -142,6 +147,7 @@ def main():
     ap.add_argument("--backend", type=int, default=0)
     ap.add_argument("--no-kkt", action="store_true")
     ap.add_argument("--pivotal", type=int, default=0, help="also time B pivotal replicates (u8, one RHS)")
+    ap.add_argument("--pack2", action="store_true", help="repack u8 designs to 2 bits at create")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     for name in args.configs.split(","):
