@@ -262,7 +262,8 @@ def run_ours(args):
     achieved = (xbytes + state_bytes) / (k2_ms / 1000.0) / 1e9
     traffic = k2_traffic(args.config + ("_pack2" if pack else ""))
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": f"k2_{S.backend}", "peak_source": peak_kind,
+            "traffic": traffic,
+            "kernel": ("k2_tc2_kernel<16,1>" if pack else "k2_tc_kernel<16,1>") if S.backend == "tc" else "k2_simt", "peak_source": peak_kind,
             "algorithmic_bytes_per_launch": xbytes + state_bytes,
             "kernel_share_of_step": stage_ms[0] / prof_total_ms}
 
