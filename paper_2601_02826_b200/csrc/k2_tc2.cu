@@ -27,6 +27,9 @@
 
 #include "k2_common.cuh"
 
+#ifndef K2TC2_SMEM_KB
+#define K2TC2_SMEM_KB 226
+#endif
 #ifndef K2TC2_CW
 #define K2TC2_CW 8   // converter warps (two per SM sub-partition: the unpack loop is latency-bound with one)
 #endif
@@ -60,11 +63,14 @@ struct Cfg2 {
   static constexpr int B_ATOM = NPAD * 128;
   static constexpr int B_BYTES = 4 * B_ATOM;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (192 * 1024) / STAGE;
   static constexpr int RMAX = RM;   // RHS slots compiled in (<= NPAD / 4)
   static constexpr int RED0 = (THREADS / 32) * RMAX * (FSQR_NPART + 1);
   static constexpr int RED_DOUBLES = RED0 > 33 * FSQR_NPART ? RED0 : 33 * FSQR_NPART;
+  // as many stages as fit: several RHS make the theta-digit B tile (4 x NPAD x 128 B) larger than
+  // the 16 KB X tile, and the X bytes in flight are what keep HBM busy
+  static constexpr int STAGES = (K2TC2_SMEM_KB * 1024 - 2048 - RED_DOUBLES * 8) / STAGE;
   static constexpr int SMEM = 1024 + STAGES * STAGE + 1024 + RED_DOUBLES * 8;
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
 __device__ __forceinline__ void umma_i8_tmem_a(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
