@@ -30,6 +30,9 @@
 #ifndef K2TC2_SMEM_KB
 #define K2TC2_SMEM_KB 226
 #endif
+#ifndef K2TC2_BATOMS
+#define K2TC2_BATOMS 4   // theta-digit atoms loaded per stage (4; fewer only in measurement variants)
+#endif
 #ifndef K2TC2_CW
 #define K2TC2_CW 8   // converter warps (two per SM sub-partition: the unpack loop is latency-bound with one)
 #endif
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
       const uint64_t pol_x = D.x_policy == 2 ? policy_evict_last()
                              : (D.x_policy == 1 ? policy_evict_normal() : policy_evict_first());
       const uint64_t pol_b = policy_evict_last();
-      const uint32_t bytes = (uint32_t)(A_BYTES + 4 * 4 * D.R * 128);
+      const uint32_t bytes = (uint32_t)(A_BYTES + K2TC2_BATOMS * 4 * D.R * 128);
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -201,7 +204,7 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
             mbar_expect_tx(&full[stage], bytes);
             tma_load_2d(sA + stage * A_BYTES, &tmX, &full[stage], kb * PK, (int)(t * TILE_M), pol_x);
 #pragma unroll
-            for (int a = 0; a < 4; ++a)
+            for (int a = 0; a < K2TC2_BATOMS; ++a)
               tma_load_2d(sB + stage * CF::B_BYTES + a * CF::B_ATOM, &tmB, &full[stage], kb * KS + a * 128, 0, pol_b);
           }
           __syncwarp();
