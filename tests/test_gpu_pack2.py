@@ -129,3 +129,42 @@ def test_k1_tcp_equals_cuda_core_forward(cuda_ok, monkeypatch, n, p, taus):
         del S
     for u, v in zip(out[0], out[1]):
         np.testing.assert_array_equal(u, v)
+
+
+def test_pack2_drivers_equal_u8(cuda_ok):
+    """The drivers built on the hot path (warm-started lambda path + HBIC, one-step LLA) give the
+    same answers on a repacked context as on the u8 one: identical iteration counts and supports,
+    beta to 1e-12.  The pivotal statistic is U8-only (FSQR_ERR_CONFIG on a repacked context)."""
+    import paper_2601_02826_b200 as fs
+
+    a = datagen.make("c2", n=700, p=1500, storage=fs.U8)
+    X, y = to_device(a)
+    eta = [25.0] * 5
+    lm = None
+    out = {}
+    for flags in (0, fs.DESIGN_PACK2):
+        S = fs.Solver(X, fs.U8, a.n, a.p, a.ld, y, [0.5], [1.0], G=5, eta=eta, tol=1e-6, max_iter_point=20000,
+                      flags=flags)
+        if lm is None:
+            lm = S.lambda_max()[0]
+        grid = np.array([[lm * 0.05 ** (t / 5) for t in range(6)]])
+        res = S.path(grid)
+        betas = [S.path_beta(0, t) for t in range(6)]
+        h = S.path_hbic(6)
+        S2 = fs.Solver(X, fs.U8, a.n, a.p, a.ld, y, [0.5], [0.1 * lm], G=5, eta=eta, tol=1e-6, max_iter=200000,
+                       flags=flags)
+        lla = S2.lla(fs.SCAD, 3.7, 1)
+        out[flags] = (res, betas, h, lla, S2.beta()[0])
+        if flags:
+            with pytest.raises(fs.FsqrError, match="ERR_CONFIG"):
+                S.pivotal(128)
+        del S, S2
+    (r0, b0, h0, l0, bl0), (r1, b1, h1, l1, bl1) = out[0], out[fs.DESIGN_PACK2]
+    np.testing.assert_array_equal(r0["iters"], r1["iters"])
+    np.testing.assert_array_equal(r0["nnz"], r1["nnz"])
+    for u, v in zip(b0, b1):
+        assert rel(v, u) < 1e-12
+        assert np.array_equal(u != 0, v != 0)
+    np.testing.assert_allclose(h1, h0, rtol=1e-12)
+    assert list(l0["stage_iters"]) == list(l1["stage_iters"])
+    assert rel(bl1, bl0) < 1e-12
