@@ -256,6 +256,9 @@ const char* fsqr_backend_name(const fsqr_ctx* ctx);
  * copies X and y to the device on `stream`, creates a context, runs `iters` iterations
  * (iters < 0: fsqr_solve), copies beta (standardised, [n_rhs][p+1]) back, destroys the
  * context and frees the copies.  X->data_dev here points to HOST memory (pinned for speed).
+ * With U8 storage and FSQR_DESIGN_PACK2 the codes travel in 256 MB column chunks through a
+ * staging buffer and are repacked on the device as they arrive: only the 2-bit design (n*p/4
+ * bytes) is ever resident; a code > 3 is FSQR_ERR_DATA.
  */
 fsqr_status fsqr_fit_host(const fsqr_design* X_host, const double* y_host, int32_t n_rhs, const double* tau_host,
                           const double* lambda_host, const fsqr_options* opt, int64_t iters, double* beta_host,

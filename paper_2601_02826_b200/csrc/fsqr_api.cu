@@ -1253,19 +1253,58 @@ fsqr_status fsqr_fit_host(const fsqr_design* Xh, const double* y_host, int32_t n
     return set_err(nullptr, e == cudaErrorMemoryAllocation ? FSQR_ERR_OOM : FSQR_ERR_CUDA, "%s: %s", what,
                    cudaGetErrorString(e));
   };
-  cudaError_t e = cudaMallocAsync(&dX, xb, st);
-  if (e != cudaSuccess) return fail("device copy of X", e);
-  e = cudaMallocAsync((void**)&dy, sizeof(double) * Xh->n, st);
-  if (e != cudaSuccess) return fail("device copy of y", e);
-  e = cudaMemcpyAsync(dX, Xh->data_dev, xb, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(dy, y_host, sizeof(double) * Xh->n, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return fail("host-to-device copy", e);
   fsqr_design Xd = *Xh;
-  Xd.data_dev = dX;
   Xd.mean_dev = nullptr;
   Xd.scale_dev = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&dy, sizeof(double) * Xh->n, st);
+  if (e != cudaSuccess) return fail("device copy of y", e);
+  e = cudaMemcpyAsync(dy, y_host, sizeof(double) * Xh->n, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return fail("host-to-device copy", e);
+  if ((Xh->flags & FSQR_DESIGN_PACK2) && Xh->storage == FSQR_U8 && Xh->data_dev && Xh->n >= 2 && Xh->n <= 65536 &&
+      Xh->p >= 1 && Xh->ld >= Xh->n && Xh->ld % 16 == 0) {
+    // u8 codes repacked on the way in: 256 MB column chunks are copied into a staging buffer and
+    // packed straight into the 2-bit design, so only n*p/4 bytes of X are ever resident
+    const int64_t ld2 = ((Xh->n + 3) / 4 + 15) / 16 * 16;
+    const int64_t cc = std::max<int64_t>(1, std::min<int64_t>(Xh->p, ((int64_t)256 << 20) / Xh->ld));
+    uint8_t* stg = nullptr;
+    int* bad = nullptr;
+    e = cudaMallocAsync(&dX, (size_t)ld2 * Xh->p, st);
+    if (e != cudaSuccess) return fail("device copy of X", e);
+    e = cudaMallocAsync((void**)&stg, (size_t)cc * Xh->ld, st);
+    if (e == cudaSuccess) e = cudaMallocAsync((void**)&bad, sizeof(int), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0, sizeof(int), st);
+    for (int64_t c0 = 0; e == cudaSuccess && c0 < Xh->p; c0 += cc) {
+      const int64_t nc = std::min(cc, Xh->p - c0);
+      e = cudaMemcpyAsync(stg, (const uint8_t*)Xh->data_dev + c0 * Xh->ld, (size_t)nc * Xh->ld, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) {
+        launch_pack2(stg, Xh->ld, (int)Xh->n, nc, (uint8_t*)dX + c0 * ld2, ld2, bad, st);
+        e = cudaGetLastError();
+      }
+    }
+    int h_bad = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (stg) cudaFreeAsync(stg, st);
+    if (bad) cudaFreeAsync(bad, st);
+    if (e != cudaSuccess) return fail("host-to-device copy / repack", e);
+    if (h_bad) {
+      cudaFreeAsync(dX, st);
+      cudaFreeAsync(dy, st);
+      cudaStreamSynchronize(st);
+      return set_err(nullptr, FSQR_ERR_DATA, "FSQR_DESIGN_PACK2: a genotype code exceeds 3");
+    }
+    Xd.storage = FSQR_PACKED2;
+    Xd.flags = 0;
+    Xd.ld = ld2;
+  } else {
+    e = cudaMallocAsync(&dX, xb, st);
+    if (e != cudaSuccess) return fail("device copy of X", e);
+    e = cudaMemcpyAsync(dX, Xh->data_dev, xb, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return fail("host-to-device copy", e);
+  }
+  Xd.data_dev = dX;
   fsqr_status s = fsqr_create(&Xd, dy, n_rhs, tau_host, lambda_host, nullptr, opt, stream, &ctx);
-  if (s == FSQR_OK && (Xh->flags & FSQR_DESIGN_PACK2)) {   // the ctx owns its packed copy
+  if (s == FSQR_OK && (Xd.flags & FSQR_DESIGN_PACK2)) {   // the ctx owns its packed copy
     cudaFreeAsync(dX, st);
     dX = nullptr;
   }

@@ -168,3 +168,24 @@ def test_pack2_drivers_equal_u8(cuda_ok):
     np.testing.assert_allclose(h1, h0, rtol=1e-12)
     assert list(l0["stage_iters"]) == list(l1["stage_iters"])
     assert rel(bl1, bl0) < 1e-12
+
+
+def test_fit_host_pack2_chunked_and_bad_code(cuda_ok):
+    """fsqr_fit_host repacks a u8 host design chunk by chunk (p large enough for several 256 MB
+    chunks is too big for a test, so the chunking is exercised through ld: one column chunk holds
+    256 MB / ld columns) and rejects a code > 3 with FSQR_ERR_DATA."""
+    import paper_2601_02826_b200 as fs
+
+    a = datagen.make("c2", n=3000, p=2500, storage=fs.U8)
+    b = datagen.make("c2", n=3000, p=2500, storage=fs.PACKED2)
+    eta = [30.0] * 5
+    ba, _ = fs.fsqr_fit_host(a.X, fs.U8, a.n, a.p, a.ld, a.y, [0.3, 0.8], [0.03, 0.03], 60,
+                             opt=fs.default_options(G=5), eta=eta, flags=fs.DESIGN_PACK2)
+    bb, _ = fs.fsqr_fit_host(b.X, fs.PACKED2, b.n, b.p, b.ld, b.y, [0.3, 0.8], [0.03, 0.03], 60,
+                             opt=fs.default_options(G=5), eta=eta)
+    np.testing.assert_array_equal(ba, bb)
+    X = a.X.copy()
+    X[2400, 17] = 9
+    with pytest.raises(fs.FsqrError, match="ERR_DATA"):
+        fs.fsqr_fit_host(X, fs.U8, a.n, a.p, a.ld, a.y, [0.5], [0.03], 10, opt=fs.default_options(G=5), eta=eta,
+                         flags=fs.DESIGN_PACK2)
