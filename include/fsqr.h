@@ -187,8 +187,8 @@ fsqr_status fsqr_lla(fsqr_ctx* ctx, int32_t penalty, double a, int32_t L, int64_
  *     Lambda_host[b] = max_{j>=1} | sum_i x~_ij (tau_rhs - 1{U_bi <= tau_rhs}) | / n.
  * 128 replicates per pass over X on the tensor cores (exact integer sums).  The conventional
  * choice is lambda = 1.1 x the 0.9 empirical quantile of Lambda (Belloni-Chernozhukov).
- * U8 storage only, as stored (a context created with FSQR_DESIGN_PACK2 streams 2-bit codes and
- * returns FSQR_ERR_CONFIG; use a second U8 context on the same X).  Blocking.
+ * Genotype storage (U8 or PACKED2; a 2-bit design is unpacked into a temporary u8 copy of n*p
+ * bytes for the duration of the call, since the tiles are streamed as bytes).  Blocking.
  */
 fsqr_status fsqr_pivotal(fsqr_ctx* ctx, int32_t rhs, int64_t B, uint64_t seed, double* Lambda_host, void* stream);
 

@@ -90,6 +90,8 @@ struct fsqr_ctx {
   int* piv_nb = nullptr;
   unsigned long long* piv_lmax = nullptr;
   CUtensorMap tmPivA{}, tmPivX{};
+  void* piv_enc = nullptr;      // cuTensorMapEncodeTiled
+  bool piv_x_ready = false;     // tmPivX describes the borrowed u8 X (not rebuilt per call)
 };
 
 namespace {
@@ -895,9 +897,11 @@ fsqr_status fsqr_pivotal(fsqr_ctx* ctx, int32_t rhs, int64_t B, uint64_t seed, d
   if (!ctx || !Lambda_host) return set_err(ctx, FSQR_ERR_CONFIG, "null argument");
   if (rhs < 0 || rhs >= ctx->R) return set_err(ctx, FSQR_ERR_CONFIG, "rhs %d out of range", rhs);
   if (B < 1) return set_err(ctx, FSQR_ERR_CONFIG, "B must be >= 1");
-  if (ctx->D.storage != FSQR_U8) return set_err(ctx, FSQR_ERR_CONFIG, "the pivotal statistic needs U8 storage");
+  if (ctx->D.storage != FSQR_U8 && ctx->D.storage != FSQR_PACKED2)
+    return set_err(ctx, FSQR_ERR_CONFIG, "the pivotal statistic needs genotype storage");
   cudaStream_t st = (cudaStream_t)stream;
   const int ldk = (int)(((ctx->n + 127) / 128) * 128);
+  const bool packed = ctx->D.storage == FSQR_PACKED2;
   if (!ctx->piv_draws) {
     AL(ctx->piv_draws, (size_t)128 * ldk);
     AL(ctx->piv_nb, 128);
@@ -918,15 +922,40 @@ fsqr_status fsqr_pivotal(fsqr_ctx* ctx, int32_t rhs, int64_t B, uint64_t seed, d
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) return set_err(ctx, FSQR_ERR_CUDA, "tensor map for the draws failed (%d)", (int)r);
     }
-    {
-      cuuint64_t dims[2] = {(cuuint64_t)ctx->n, (cuuint64_t)ctx->p};
-      cuuint64_t strides[1] = {(cuuint64_t)ctx->D.ld};
-      cuuint32_t box[2] = {128, 256};
-      CUresult r = enc(&ctx->tmPivX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)ctx->D.X8, dims, strides, box, es,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r != CUDA_SUCCESS) return set_err(ctx, FSQR_ERR_CUDA, "tensor map for X (256 rows) failed (%d)", (int)r);
+    ctx->piv_enc = fn;
+  }
+  // X as u8 tiles of 256 columns x 128 samples.  A 2-bit design is unpacked into a temporary u8
+  // copy for the duration of the call (the statistic is a one-off tuning step, not the hot loop).
+  const uint8_t* x8 = ctx->D.X8;
+  int64_t ld8 = ctx->D.ld;
+  uint8_t* tmp = nullptr;
+  struct TmpFree {   // the temporary copy goes on every exit path
+    uint8_t** p;
+    cudaStream_t s;
+    ~TmpFree() {
+      if (*p) {
+        cudaFreeAsync(*p, s);
+        cudaStreamSynchronize(s);
+      }
     }
+  } tmp_guard{&tmp, st};
+  if (packed) {
+    ld8 = (ctx->n + 15) / 16 * 16;
+    CK(cudaMallocAsync((void**)&tmp, (size_t)ld8 * ctx->p, st));
+    launch_unpack2(ctx->D.X8, ctx->D.ld, ctx->p, tmp, ld8, st);
+    CK(cudaGetLastError());
+    x8 = tmp;
+  }
+  if (packed || !ctx->piv_x_ready) {
+    cuuint32_t es[2] = {1, 1};
+    cuuint64_t dims[2] = {(cuuint64_t)ctx->n, (cuuint64_t)ctx->p};
+    cuuint64_t strides[1] = {(cuuint64_t)ld8};
+    cuuint32_t box[2] = {128, 256};
+    CUresult r = ((EncodeTiledFn)ctx->piv_enc)(&ctx->tmPivX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)x8, dims, strides,
+                                               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(ctx, FSQR_ERR_CUDA, "tensor map for X (256 rows) failed (%d)", (int)r);
+    ctx->piv_x_ready = !packed;
   }
   const int grid = (int)std::min<int64_t>((ctx->p + 255) / 256, ctx->sms);
   std::vector<unsigned long long> h(128);

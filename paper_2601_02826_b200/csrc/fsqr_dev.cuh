@@ -485,6 +485,7 @@ void launch_k1(const Dev& D, int grid, cudaStream_t st);
 void launch_finalize(const Dev& D, cudaStream_t st);
 void launch_pack2(const uint8_t* x8, int64_t ld8, int n, int64_t p, uint8_t* x2, int64_t ld2, int* bad,
                   cudaStream_t st);
+void launch_unpack2(const uint8_t* x2, int64_t ld2, int64_t p, uint8_t* x8, int64_t ld8, cudaStream_t st);
 int k2_tc_smem_bytes(int npad);
 cudaError_t k2_tc_init();
 cudaError_t k1_init();

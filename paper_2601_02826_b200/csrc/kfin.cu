@@ -832,6 +832,28 @@ void launch_finalize(const Dev& D, cudaStream_t st) {
   else
     launch_pdl(k_finalize_mc, dim3((D.n + FIN_THREADS - 1) / FIN_THREADS, D.R), dim3(FIN_THREADS), 0, st, D);
 }
+// PACKED2 -> u8 (the pivotal statistic streams u8 tiles): one thread per packed word, 16 codes out
+static __global__ void k_unpack2(const uint32_t* __restrict__ x2, int64_t ld2, int64_t p, uint8_t* __restrict__ x8,
+                          int64_t ld8) {
+  const int64_t wpc = ld8 / 16;   // 16-sample output groups per column
+  const int64_t total = p * wpc;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = w / wpc, j = w - c * wpc;
+    const uint32_t v = x2[(c * ld2) / 4 + j];
+    uint32_t o[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t y = (v >> (8 * b)) & 0xFFu;
+      o[b] = (y & 3u) | (((y >> 2) & 3u) << 8) | (((y >> 4) & 3u) << 16) | (((y >> 6) & 3u) << 24);
+    }
+    *reinterpret_cast<uint4*>(x8 + c * ld8 + 16 * j) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+void launch_unpack2(const uint8_t* x2, int64_t ld2, int64_t p, uint8_t* x8, int64_t ld8, cudaStream_t st) {
+  k_unpack2<<<148 * 8, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(x2), ld2, p, x8, ld8);
+}
+
 void launch_pack2(const uint8_t* x8, int64_t ld8, int n, int64_t p, uint8_t* x2, int64_t ld2, int* bad,
                   cudaStream_t st) {
   k_pack2<<<148 * 8, 256, 0, st>>>(x8, ld8, n, p, reinterpret_cast<uint32_t*>(x2), ld2, bad);
