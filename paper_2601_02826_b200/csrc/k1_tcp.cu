@@ -29,6 +29,15 @@
 
 #include "fsqr_dev.cuh"
 
+#ifndef K1P_RTMAX
+#define K1P_RTMAX 16   // row tiles per slab cap (measurement knob)
+#endif
+#ifndef K1P_SMEM_KB
+#define K1P_SMEM_KB 220
+#endif
+#ifndef K1P_CTAS
+#define K1P_CTAS 1     // CTAs per SM the launch grid assumes
+#endif
 #ifndef K1P_DBG
 #define K1P_DBG 0   // measurement variants: bit 0 skips the MMAs, bit 1 the unpack, bit 2 the loads, bit 3 the atomics
 #endif
@@ -45,7 +54,8 @@ template <int RMAX>
 struct K1P {
   static constexpr int NDIG = 6 * RMAX;
   static constexpr int N = NDIG <= 16 ? 16 : (NDIG <= 32 ? 32 : (NDIG <= 48 ? 48 : 96));
-  static constexpr int RT = N <= 32 ? 16 : (N <= 48 ? 8 : 4);   // row tiles per slab (RT * N <= 512)
+  static constexpr int RT0 = N <= 32 ? 16 : (N <= 48 ? 8 : 4);  // row tiles per slab (RT * N <= 512)
+  static constexpr int RT = RT0 < K1P_RTMAX ? RT0 : K1P_RTMAX;
   static constexpr int SR = 128 * RT;                          // rows per slab
   static constexpr int SEGB = SR / 4;                          // packed bytes per column segment
   static constexpr int UPL = RT / 4;                           // 16-byte units per lane per chunk
@@ -55,7 +65,7 @@ struct K1P {
   static constexpr int ABUF = RT * ATILE;
   static constexpr int MB = RMAX <= 4 ? 256 : 128;             // metadata entries per block
   static constexpr int META = 2 * MB * (4 + 8 * RMAX);         // two blocks: colsum, beta/s
-  static constexpr int SD0 = (220 * 1024 - NAB * ABUF - SB * BTILE - META) / DSTAGE;
+  static constexpr int SD0 = (K1P_SMEM_KB * 1024 - NAB * ABUF - SB * BTILE - META) / DSTAGE;
   static constexpr int SD = SD0 < 2 ? 2 : (SD0 > 6 ? 6 : SD0); // data ring depth (chunks)
   static constexpr int TCOLS = RT * N <= 256 ? 256 : 512;
   static constexpr int SMEM = 1024 + NAB * ABUF + SD * DSTAGE + SB * BTILE + META + 1024;
@@ -109,7 +119,7 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
 }
 
 template <int RMAX>
-__global__ void __launch_bounds__(THREADS, 1) k1_tcp_kernel(const Dev D, int cur) {
+__global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, int cur) {
   using T = K1P<RMAX>;
   constexpr int RT = T::RT, SR = T::SR, SEGB = T::SEGB, N = T::N, SD = T::SD, NAB = T::NAB, MB = T::MB;
   constexpr int UPL = T::UPL;
@@ -452,7 +462,7 @@ cudaError_t init_one() {
 
 template <int RMAX>
 void launch_r(const Dev& D, int grid, cudaStream_t st, int cur) {
-  launch_pdl(k1_tcp_kernel<RMAX>, dim3(grid), dim3(THREADS), K1P<RMAX>::SMEM, st, D, cur);
+  launch_pdl(k1_tcp_kernel<RMAX>, dim3(grid * K1P_CTAS), dim3(THREADS), K1P<RMAX>::SMEM, st, D, cur);
 }
 
 }  // namespace
