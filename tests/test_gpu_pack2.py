@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 import datagen
+import oracle
 from gpu_helpers import rel, to_device
 
 pytestmark = pytest.mark.gpu
@@ -188,3 +189,27 @@ def test_fit_host_pack2_chunked_and_bad_code(cuda_ok):
     with pytest.raises(fs.FsqrError, match="ERR_DATA"):
         fs.fsqr_fit_host(X, fs.U8, a.n, a.p, a.ld, a.y, [0.5], [0.03], 10, opt=fs.default_options(G=5), eta=eta,
                          flags=fs.DESIGN_PACK2)
+
+
+@pytest.mark.parametrize("n,p,G,taus", [(37, 1, 1, [0.5]), (130, 3, 2, [0.3, 0.7]), (513, 129, 5, [0.5]),
+                                        (1023, 700, 5, list(np.linspace(0.05, 0.95, 16))), (2, 7, 1, [0.5])])
+def test_pack2_flag_parity_ragged(cuda_ok, n, p, G, taus):
+    """FSQR_DESIGN_PACK2 on ragged and tiny shapes (n not a multiple of 4, 16, 128 or 512; a
+    single column; the maximum 16 RHS) against the fp64 oracle run on the same u8 codes."""
+    import paper_2601_02826_b200 as fs
+
+    prob = datagen.make("c2", n=n, p=p, storage=fs.U8)
+    d = oracle.Design.from_problem(prob)
+    mu = 2.0 / prob.n
+    eta = oracle.eta(d, G, mu)
+    lams = [0.05 * oracle.lambda_max(d, prob.y, t)[0] for t in taus]
+    X, y = to_device(prob)
+    S = fs.Solver(X, fs.U8, prob.n, prob.p, prob.ld, y, taus, lams, G=G, mu=mu, eta=eta, flags=fs.DESIGN_PACK2)
+    k = 60
+    S.iterate(k)
+    b, z, t = S.state()
+    for r in sorted({0, len(taus) // 2, len(taus) - 1}):
+        o = oracle.solve(d, prob.y, taus[r], oracle.lam_vector(prob.p, lams[r]), eta, mu, G, max_iter=k, check=False)
+        assert rel(b[r], o["beta"]) < 1e-6, r
+        assert rel(t[r], o["theta"]) < 1e-6, r
+        assert np.array_equal(b[r] != 0, o["beta"] != 0), r
