@@ -488,6 +488,8 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
   D.x_policy = 0;
   if (const char* ev = getenv("FSQR_X_POLICY")) D.x_policy = atoi(ev);
   if (const char* ev = getenv("FSQR_K1_POLICY")) D.k1_policy = atoi(ev);
+  D.k1_esmax = 65536;
+  if (const char* ev = getenv("FSQR_K1_ESMAX")) D.k1_esmax = std::max(32, std::min(65536, atoi(ev) / 32 * 32));
   D.ldk = (int)(((X->n + 127) / 128) * 128);
   D.X8 = X->storage != 0 ? (const uint8_t*)X->data_dev : nullptr;
   D.Xf = X->storage == 0 ? (const float*)X->data_dev : nullptr;

@@ -31,6 +31,7 @@ enum { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_NUMERIC = 3 };
 struct Dev {
   // sizes / layout
   int n, R, G, storage, npad, ldk;
+  int k1_esmax;                     // k1_tcp: support entries per work item cap (<= 65536; FSQR_K1_ESMAX, tests)
   int k1_tc;                        // forward product: 0 k1_bulk (CUDA cores), 1 k1_tc (TMEM transpose), 2 k1_tcg (gather4), 3 k1_tcp (2-bit, smem unpack)
   const void* tmG;                  // host pointer to the gather4 tensor map (launcher side only)
   int x_policy;                     // L2 hint of the X stream in K2: 0 evict_first, 1 normal, 2 evict_last

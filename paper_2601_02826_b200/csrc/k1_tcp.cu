@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
   // |code 4^q| <= 192, |digit| <= 128, 192 * 128 * 2^16 < 2^31)
   const int per = max(1, (int)gridDim.x / nslab);
   int64_t es = ((int64_t)max(cnt, 1) + per - 1) / per;
-  es = min((int64_t)65536, ((es + KC - 1) / KC) * KC);
+  es = min((int64_t)D.k1_esmax, ((es + KC - 1) / KC) * KC);
   const int64_t nsl = ((int64_t)cnt + es - 1) / es;
   const int64_t nwork = skip ? 0 : nsl * nslab;
 

@@ -213,3 +213,27 @@ def test_pack2_flag_parity_ragged(cuda_ok, n, p, G, taus):
         assert rel(b[r], o["beta"]) < 1e-6, r
         assert rel(t[r], o["theta"]) < 1e-6, r
         assert np.array_equal(b[r] != 0, o["beta"] != 0), r
+
+
+@pytest.mark.parametrize("esmax,taus", [(64, [0.5]), (96, [0.2, 0.6, 0.9]), (32, [k / 10 for k in range(1, 10)])])
+def test_k1_tcp_many_work_items_per_cta(cuda_ok, monkeypatch, esmax, taus):
+    """Full support (lambda = 0) with the per-item entry cap lowered (FSQR_K1_ESMAX) so every
+    CTA of k1_tcp runs many work items in a row: the metadata ring, the per-item cp.async
+    pipeline and the accumulator hand-off across items must give the CUDA-core kernel's sums."""
+    import paper_2601_02826_b200 as fs
+
+    b = datagen.make("c4", n=1100, p=3000, storage=fs.PACKED2)
+    X, y = to_device(b)
+    eta = [40.0] * 5
+    out = []
+    for mode in ("bulk", "tcp"):
+        monkeypatch.setenv("FSQR_K1", mode)
+        monkeypatch.setenv("FSQR_K1_ESMAX", str(esmax))
+        S = fs.Solver(X, fs.PACKED2, b.n, b.p, b.ld, y, taus, [0.0] * len(taus), G=5, eta=eta)
+        S.iterate(25)
+        st = S.state()
+        assert int(S.trace(1)[-1, 0, 4]) > 2000   # most columns in the support
+        out.append(st + (S.objective(),))
+        del S
+    for u, v in zip(out[0], out[1]):
+        np.testing.assert_array_equal(u, v)
