@@ -30,6 +30,9 @@
 #ifndef K2TC2_SMEM_KB
 #define K2TC2_SMEM_KB 226
 #endif
+#ifndef K2TC2_NOMMA
+#define K2TC2_NOMMA 0   // measurement variant: skip the MMAs (wrong results)
+#endif
 #ifndef K2TC2_BATOMS
 #define K2TC2_BATOMS 4   // theta-digit atoms loaded per stage (4; fewer only in measurement variants)
 #endif
@@ -45,12 +48,16 @@ constexpr int KS = 4 * PK;                // samples (K) per stage
 constexpr int A_BYTES = TILE_M * PK;      // 16 KB packed A per stage
 constexpr int A_COLS = KS / 4;            // TMEM columns per A buffer (4 int8 per 32-bit cell)
 
-// warps: 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4..4+CW-1 convert, then 4 epilogue warps.  One RHS
+// warps: 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4..4+CW-1 convert, then EW epilogue warps.  One RHS
 // (the C4 workload) keeps few registers per thread, so it affords 8 converter warps (two per SM
 // sub-partition: the unpack loop is latency-bound with one); more RHS keep 4.
 template <int NPAD, int RM>
 struct Cfg2 {
-  static constexpr int CW = K2TC2_CW;
+  // up to 4 RHS: 8 converter warps, 4 epilogue warps; more: the per-column epilogue (E14, KKT
+  // partials and support entries for every RHS) is the slower side, so 4 converters and two sets
+  // of 4 epilogue warps taking alternate tiles (one accumulator buffer each)
+  static constexpr int CW = NPAD == 16 ? K2TC2_CW : 4;   // (4 converters at NPAD = 16 would spill)
+  static constexpr int EW = NPAD == 16 ? 4 : 8;
   // NPAD == 16: one accumulator per code plane q, so the converter can leave the codes in place
   // ((w & (3 << 2q)) = x * 4^q, one LOP per word instead of shift + mask); the epilogue divides
   // each plane's exact sum by 4^q.  Needs 2 x 4 x 16 = 128 TMEM columns.
@@ -62,7 +69,7 @@ struct Cfg2 {
   static constexpr int A_COL0 = 2 * ACC_COLS;                     // A buffers after the two accumulators
   static constexpr int NAB = (512 - A_COL0) / A_COLS < 3 ? (512 - A_COL0) / A_COLS : 3;   // TMEM A buffers
   static_assert(NAB >= 2, "TMEM budget");
-  static constexpr int THREADS = 32 * (8 + CW);
+  static constexpr int THREADS = 32 * (4 + CW + EW);
   static constexpr int B_ATOM = NPAD * 128;
   static constexpr int B_BYTES = 4 * B_ATOM;
   static constexpr int STAGE = A_BYTES + B_BYTES;
@@ -242,7 +249,7 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
               const uint32_t dq = CF::SPLITQ ? d_tmem + (uint32_t)((kk >> 2) * NPAD)
                                              : d_tmem + (uint32_t)(((kk >> 2) & 1) * NPAD);
               const bool accum = CF::SPLITQ ? (kb != 0 || (kk & 3) != 0) : (kb != 0 || (kk & 11) != 0);   // first of each group: kk = 0, 4
-              umma_i8_tmem_a(dq, a_tmem + (uint32_t)(8 * kk),
+              if (!K2TC2_NOMMA) umma_i8_tmem_a(dq, a_tmem + (uint32_t)(8 * kk),
                              bdesc0 + (uint64_t)((kk >> 2) * (CF::B_ATOM >> 4) + 2 * (kk & 3)), idesc, accum);
             }
             umma_commit(&empty[stage]);
@@ -321,9 +328,11 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
   } else if (wid >= EPI0) {
     // ===== epilogue: TMEM lanes 32*(wid%4) .. +31 = columns of the tile =====
     const int q = wid & 3;
+    const int eset = (wid - EPI0) >> 2;   // 0, or 0/1 with two epilogue sets (alternate tiles)
     int lt = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
       const int acc = lt & 1;
+      if (CF::EW == 8 && acc != eset) continue;
       const uint32_t aph = (lt >> 1) & 1;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
