@@ -522,24 +522,27 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
   }
   ctx->k1_grid = ctx->sms;   // k1_bulk scales by its resident CTAs per SM; k1_tc runs one CTA per SM
   CK(k1_init());
-  // forward-product kernel: with 3+ RHS the CUDA-core kernel's 2R multiply-adds per element lose
-  // to the gather4 tensor-core kernel (C5 at 0.05 lambda_max: 0.80 vs 2.43 ms); with 1-2 RHS the
-  // gather's one TMA operation per 512 bytes is the slower side (M: 140 vs 55 us).
-  // FSQR_K1=bulk|tc|gather overrides, for measurements.
+  // forward-product kernel.  History: with 3+ RHS the CUDA-core k1_bulk's 2R multiply-adds per
+  // element lost to the gather4 tensor-core kernel (C5 at 0.05 lambda_max: 0.80 vs 2.43 ms), whose
+  // one TMA operation per 512 bytes made it the slower one for 1-2 RHS (M: 140 vs 55 us).
+  // FSQR_K1=bulk|tc|gather|tcp|tcu overrides, for measurements.
+  // k1_tcp (tensor cores, A tile built on chip from per-lane cp.async) beats both for genotype
+  // storage: 2-bit M 53 -> 29 us and C4 210 -> 104 us (in-place code planes); u8 M 59 -> 54 us,
+  // C2 3 RHS 31 -> 14 us, C5 9 RHS 18.5 -> 14.4 us against the gather kernel.
   D.k1_tc = 0;
-  if (ctx->backend == FSQR_BACKEND_TC && X->storage == FSQR_U8 && R >= 3) D.k1_tc = 2;
-  // 2-bit storage: unpack on chip into the tensor-core A tile (M: 53 -> 29 us, C4: 210 -> 104 us)
+  if (ctx->backend == FSQR_BACKEND_TC && X->storage == FSQR_U8) D.k1_tc = 4;
   if (ctx->backend == FSQR_BACKEND_TC && X->storage == FSQR_PACKED2) D.k1_tc = 3;
   if (const char* ev = getenv("FSQR_K1")) {
     if (!strcmp(ev, "bulk")) D.k1_tc = 0;
     else if (!strcmp(ev, "tc") && X->storage != FSQR_F32_DENSE) D.k1_tc = 1;
     else if (!strcmp(ev, "gather") && X->storage == FSQR_U8) D.k1_tc = 2;
     else if (!strcmp(ev, "tcp") && X->storage == FSQR_PACKED2) D.k1_tc = 3;
+    else if (!strcmp(ev, "tcu") && X->storage == FSQR_U8) D.k1_tc = 4;
 
   }
   if (D.k1_tc == 1) CK(k1_tc_init());
   if (D.k1_tc == 2) CK(k1_tcg_init());
-  if (D.k1_tc == 3) CK(k1_tcp_init());
+  if (D.k1_tc == 3 || D.k1_tc == 4) CK(k1_tcp_init());
 
   // ---------------- allocations
   int32_t* colsum;

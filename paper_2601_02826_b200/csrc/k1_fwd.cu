@@ -428,7 +428,7 @@ void launch_k1_mode(const Dev& D, int grid, cudaStream_t st, int cur) {
     launch_k1_tcg(D, D.tmG, grid, st, cur);
     return;
   }
-  if (D.k1_tc == 3 && D.storage == 2) {
+  if ((D.k1_tc == 3 && D.storage == 2) || (D.k1_tc == 4 && D.storage == 1)) {
     launch_k1_tcp(D, grid, st, cur);
     return;
   }

@@ -50,23 +50,23 @@ constexpr int THREADS = 32 * (4 + CW);
 constexpr int ATILE = 128 * KC; // one row tile x one chunk: 4 KB (four 1 KB swizzle atoms)
 constexpr int SB = 4;           // B tile ring
 
-template <int RMAX>
+template <int RMAX, int ST>
 struct K1P {
   static constexpr int NDIG = 6 * RMAX;
   static constexpr int N = NDIG <= 16 ? 16 : (NDIG <= 32 ? 32 : (NDIG <= 48 ? 48 : 96));
   static constexpr int RT0 = N <= 32 ? 16 : (N <= 48 ? 8 : 4);  // row tiles per slab (RT * N <= 512)
   static constexpr int RT = RT0 < K1P_RTMAX ? RT0 : K1P_RTMAX;
   static constexpr int SR = 128 * RT;                          // rows per slab
-  static constexpr int SEGB = SR / 4;                          // packed bytes per column segment
-  static constexpr int UPL = RT / 4;                           // 16-byte units per lane per chunk
-  static constexpr int DSTAGE = KC * SEGB;                     // one chunk of packed segments
+  static constexpr int SEGB = ST == 1 ? SR : SR / 4;           // bytes per column segment
+  static constexpr int UPL = ST == 1 ? RT : RT / 4;            // 16-byte units per lane per chunk
+  static constexpr int DSTAGE = ST == 1 ? 0 : KC * SEGB;       // one chunk of packed segments (2-bit)
   static constexpr int BTILE = N * KC;
-  static constexpr int NAB = 2;                                // A tile buffers
+  static constexpr int NAB = ST == 1 ? 3 : 2;                  // A tile buffers (u8: the copy ring)
   static constexpr int ABUF = RT * ATILE;
   static constexpr int MB = RMAX <= 4 ? 256 : 128;             // metadata entries per block
   static constexpr int META = 2 * MB * (4 + 8 * RMAX);         // two blocks: colsum, beta/s
-  static constexpr int SD0 = (K1P_SMEM_KB * 1024 - NAB * ABUF - SB * BTILE - META) / DSTAGE;
-  static constexpr int SD = SD0 < 2 ? 2 : (SD0 > 6 ? 6 : SD0); // data ring depth (chunks)
+  static constexpr int SD0 = ST == 1 ? 0 : (K1P_SMEM_KB * 1024 - NAB * ABUF - SB * BTILE - META) / (DSTAGE ? DSTAGE : 1);
+  static constexpr int SD = ST == 1 ? 0 : (SD0 < 2 ? 2 : (SD0 > 6 ? 6 : SD0));   // 2-bit data ring depth (chunks)
   static constexpr int TCOLS = RT * N <= 256 ? 256 : 512;
   static constexpr int SMEM = 1024 + NAB * ABUF + SD * DSTAGE + SB * BTILE + META + 1024;
   static_assert(RT * N <= 512, "TMEM budget");
@@ -118,9 +118,9 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
-template <int RMAX>
+template <int RMAX, int ST>
 __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, int cur) {
-  using T = K1P<RMAX>;
+  using T = K1P<RMAX, ST>;
   constexpr int RT = T::RT, SR = T::SR, SEGB = T::SEGB, N = T::N, SD = T::SD, NAB = T::NAB, MB = T::MB;
   constexpr int UPL = T::UPL;
   extern __shared__ uint8_t k1p_raw[];
@@ -178,7 +178,8 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
   // |code 4^q| <= 192, |digit| <= 128, 192 * 128 * 2^16 < 2^31)
   const int per = max(1, (int)gridDim.x / nslab);
   int64_t es = ((int64_t)max(cnt, 1) + per - 1) / per;
-  es = min((int64_t)D.k1_esmax, ((es + KC - 1) / KC) * KC);
+  // (u8 codes up to 255: 255 * 128 * 2^15 < 2^31, so at most 2^15 entries per item there)
+  es = min((int64_t)min(D.k1_esmax, ST == 1 ? 32768 : 65536), ((es + KC - 1) / KC) * KC);
   const int64_t nsl = ((int64_t)cnt + es - 1) / es;
   const int64_t nwork = skip ? 0 : nsl * nslab;
 
@@ -317,6 +318,7 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
     const int32_t* sidx = D.sup_idx[par];
     int ab = 0;
     uint32_t aphase = 0, tph = 0;
+    long long ga = 0;   // u8: chunks handed to the MMA so far (A-buffer ring position)
     for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
       const int slab = (int)(w % nslab);
       const int64_t e0 = (w / nslab) * es, e1 = min((int64_t)cnt, e0 + es);
@@ -347,70 +349,120 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) ix[kk] = __shfl_sync(0xffffffffu, bi[kk], (int)(c & 31));
       };
-      auto issue = [&](int64_t c, const int (&ix)[4]) {
-        const uint32_t slot = sD0 + (uint32_t)((c % SD) * T::DSTAGE + 4 * cw * SEGB);
+      if constexpr (ST == 1) {
+        // u8: the codes are already bytes, so each lane's cp.async lands straight in the swizzled
+        // A tile (16 samples = one 16-byte chunk: row k, chunk c at c ^ (k & 7)); the A buffers
+        // are the copy ring, NAB - 1 chunks ahead.  Chunk c of the item is global chunk ga + c
+        // (buffer (ga + c) % NAB), the order the MMA warp consumes them in.
+        auto issue_u8 = [&](int64_t c, const int (&ix)[4]) {
+          const long long G = ga + c;
+          const int buf = (int)(G % NAB);
+          mbar_wait(&aempty[buf], (uint32_t)(((G / NAB) & 1) ^ 1));   // MMA of chunk G - NAB done
+          const uint32_t abuf = sA0 + (uint32_t)(buf * T::ABUF);
 #pragma unroll
-        for (int i = 0; i < UPL; ++i) {
-          const int u = i * 32 + lane, kk = u / (2 * RT), off = 16 * (u % (2 * RT));
-          int col = ix[0];   // ix[kk] without a local-memory array for lane-dependent kk
+          for (int i = 0; i < UPL; ++i) {
+            const int u = i * 32 + lane, kk = u / (SEGB / 16), off = 16 * (u % (SEGB / 16));
+            const int k = 4 * cw + kk, t = off >> 7, c16 = (off >> 4) & 7;
+            int col = ix[0];
 #pragma unroll
-          for (int q = 1; q < 4; ++q)
-            if (kk == q) col = ix[q];
-          if (!(K1P_DBG & 4) && col >= 0 && off < bytes)
-            cp_async16(slot + (uint32_t)(kk * SEGB + off), xs + (int64_t)col * D.ld + off);
-        }
-        cp_async_commit();
-      };
+            for (int q = 1; q < 4; ++q)
+              if (kk == q) col = ix[q];
+            if (!(K1P_DBG & 4) && col >= 0 && off < bytes)
+              cp_async16(abuf + (uint32_t)(t * ATILE + k * 128 + ((c16 ^ (k & 7)) << 4)),
+                         xs + (int64_t)col * D.ld + off);
+          }
+          cp_async_commit();
+        };
 #pragma unroll 1
-      for (int c = 0; c < SD - 1; ++c) {
-        int ix[4];
-        get_idx(c, ix);
-        issue(c, ix);
-      }
-      for (int64_t c = 0; c < nch; ++c) {
-        {
+        for (int c = 0; c < NAB - 1; ++c) {
+          if (c < nch) {
+            int ix[4];
+            get_idx(c, ix);
+            issue_u8(c, ix);
+          } else {
+            cp_async_commit();
+          }
+        }
+        for (int64_t c = 0; c < nch; ++c) {
+          if (c + NAB - 1 < nch) {
+            int ix[4];
+            get_idx(c + NAB - 1, ix);
+            issue_u8(c + NAB - 1, ix);
+          } else {
+            cp_async_commit();
+          }
+          cp_async_wait<NAB - 1>();   // this lane's pieces of chunk c are in the tile
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&afull[(int)((ga + c) % NAB)]);
+        }
+        ga += nch;
+      } else {
+        auto issue = [&](int64_t c, const int (&ix)[4]) {
+          const uint32_t slot = sD0 + (uint32_t)((c % SD) * T::DSTAGE + 4 * cw * SEGB);
+  #pragma unroll
+          for (int i = 0; i < UPL; ++i) {
+            const int u = i * 32 + lane, kk = u / (2 * RT), off = 16 * (u % (2 * RT));
+            int col = ix[0];   // ix[kk] without a local-memory array for lane-dependent kk
+  #pragma unroll
+            for (int q = 1; q < 4; ++q)
+              if (kk == q) col = ix[q];
+            if (!(K1P_DBG & 4) && col >= 0 && off < bytes)
+              cp_async16(slot + (uint32_t)(kk * SEGB + off), xs + (int64_t)col * D.ld + off);
+          }
+          cp_async_commit();
+        };
+  #pragma unroll 1
+        for (int c = 0; c < SD - 1; ++c) {
           int ix[4];
-          get_idx(c + SD - 1, ix);
-          issue(c + SD - 1, ix);
+          get_idx(c, ix);
+          issue(c, ix);
         }
-        cp_async_wait<SD - 1>();   // this lane's pieces of chunk c have landed
-        mbar_wait(&aempty[ab], aphase ^ 1);
-        const uint32_t src = sD0 + (uint32_t)((c % SD) * T::DSTAGE + 4 * cw * SEGB);
-        const uint32_t abuf = sA0 + (uint32_t)(ab * T::ABUF);
-#pragma unroll
-        for (int i = 0; i < ((K1P_DBG & 2) ? 0 : UPL); ++i) {
-          const int u = i * 32 + lane, kk = u / (2 * RT), off = 16 * (u % (2 * RT));
-          const int k = 4 * cw + kk, t = off >> 5, h = (off >> 4) & 1;
-          uint32_t a, b, cc, d;
-          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(a), "=r"(b), "=r"(cc), "=r"(d)
-                       : "r"(src + (uint32_t)(kk * SEGB + off)));
-          // rotate by t & 3: step jj stores word (jj + t) & 3
-          if (t & 1) {
-            const uint32_t x = a;
-            a = b, b = cc, cc = d, d = x;
+        for (int64_t c = 0; c < nch; ++c) {
+          {
+            int ix[4];
+            get_idx(c + SD - 1, ix);
+            issue(c + SD - 1, ix);
           }
-          if (t & 2) {
-            uint32_t x = a;
-            a = cc, cc = x;
-            x = b, b = d, d = x;
+          cp_async_wait<SD - 1>();   // this lane's pieces of chunk c have landed
+          mbar_wait(&aempty[ab], aphase ^ 1);
+          const uint32_t src = sD0 + (uint32_t)((c % SD) * T::DSTAGE + 4 * cw * SEGB);
+          const uint32_t abuf = sA0 + (uint32_t)(ab * T::ABUF);
+  #pragma unroll
+          for (int i = 0; i < ((K1P_DBG & 2) ? 0 : UPL); ++i) {
+            const int u = i * 32 + lane, kk = u / (2 * RT), off = 16 * (u % (2 * RT));
+            const int k = 4 * cw + kk, t = off >> 5, h = (off >> 4) & 1;
+            uint32_t a, b, cc, d;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(a), "=r"(b), "=r"(cc), "=r"(d)
+                         : "r"(src + (uint32_t)(kk * SEGB + off)));
+            // rotate by t & 3: step jj stores word (jj + t) & 3
+            if (t & 1) {
+              const uint32_t x = a;
+              a = b, b = cc, cc = d, d = x;
+            }
+            if (t & 2) {
+              uint32_t x = a;
+              a = cc, cc = x;
+              x = b, b = d, d = x;
+            }
+            const uint32_t wv[4] = {a, b, cc, d};
+            const uint32_t row = abuf + (uint32_t)(t * ATILE + k * 128);
+  #pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              const uint32_t ch = (uint32_t)(4 * h + ((jj + t) & 3));
+              const uint32_t x = wv[jj];
+              sts128(row + ((ch ^ (uint32_t)(k & 7)) << 4), x & 0x03030303u, x & 0x0C0C0C0Cu, x & 0x30303030u,
+                     x & 0xC0C0C0C0u);
+            }
           }
-          const uint32_t wv[4] = {a, b, cc, d};
-          const uint32_t row = abuf + (uint32_t)(t * ATILE + k * 128);
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const uint32_t ch = (uint32_t)(4 * h + ((jj + t) & 3));
-            const uint32_t x = wv[jj];
-            sts128(row + ((ch ^ (uint32_t)(k & 7)) << 4), x & 0x03030303u, x & 0x0C0C0C0Cu, x & 0x30303030u,
-                   x & 0xC0C0C0C0u);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&afull[ab]);
+          if (++ab == NAB) {
+            ab = 0;
+            aphase ^= 1;
           }
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&afull[ab]);
-        if (++ab == NAB) {
-          ab = 0;
-          aphase ^= 1;
         }
       }
       cp_async_wait<0>();
@@ -418,9 +470,9 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
       mbar_wait(tfull, tph);
       tph ^= 1;
       tc_fence_after();
-      const int m = q4 * 32 + lane;                     // TMEM lane of the row tile
-      const int qs = (m >> 2) & 3;                      // plane: scale 4^qs
-      const int rin = (m & ~15) | ((m & 3) << 2) | qs;  // row within the tile
+      const int m = q4 * 32 + lane;                                  // TMEM lane of the row tile
+      const int qs = ST == 1 ? 0 : (m >> 2) & 3;                     // 2-bit plane: scale 4^qs
+      const int rin = ST == 1 ? m : ((m & ~15) | ((m & 3) << 2) | qs);   // row within the tile
 #pragma unroll 1
       for (int t = hsel; t < RT; t += CW / 4) {
         const int row = slab * SR + t * 128 + rin;
@@ -455,32 +507,40 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
   }
 }
 
-template <int RMAX>
+template <int RMAX, int ST>
 cudaError_t init_one() {
-  return cudaFuncSetAttribute(k1_tcp_kernel<RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, K1P<RMAX>::SMEM);
+  return cudaFuncSetAttribute(k1_tcp_kernel<RMAX, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              K1P<RMAX, ST>::SMEM);
 }
 
-template <int RMAX>
+template <int RMAX, int ST>
 void launch_r(const Dev& D, int grid, cudaStream_t st, int cur) {
-  launch_pdl(k1_tcp_kernel<RMAX>, dim3(grid * K1P_CTAS), dim3(THREADS), K1P<RMAX>::SMEM, st, D, cur);
+  launch_pdl(k1_tcp_kernel<RMAX, ST>, dim3(grid * K1P_CTAS), dim3(THREADS), K1P<RMAX, ST>::SMEM, st, D, cur);
+}
+
+template <int ST>
+void launch_st(const Dev& D, int grid, cudaStream_t st, int cur) {
+  if (D.R <= 1) launch_r<1, ST>(D, grid, st, cur);
+  else if (D.R <= 2) launch_r<2, ST>(D, grid, st, cur);
+  else if (D.R <= 4) launch_r<4, ST>(D, grid, st, cur);
+  else if (D.R <= 8) launch_r<8, ST>(D, grid, st, cur);
+  else launch_r<16, ST>(D, grid, st, cur);
 }
 
 }  // namespace
 
 cudaError_t k1_tcp_init() {
   cudaError_t e;
-  if ((e = init_one<1>()) != cudaSuccess) return e;
-  if ((e = init_one<2>()) != cudaSuccess) return e;
-  if ((e = init_one<4>()) != cudaSuccess) return e;
-  if ((e = init_one<8>()) != cudaSuccess) return e;
-  return init_one<16>();
+#define K1TCP_INIT(R)                                              \
+  if ((e = init_one<R, 1>()) != cudaSuccess) return e;             \
+  if ((e = init_one<R, 2>()) != cudaSuccess) return e;
+  K1TCP_INIT(1) K1TCP_INIT(2) K1TCP_INIT(4) K1TCP_INIT(8) K1TCP_INIT(16)
+#undef K1TCP_INIT
+  return cudaSuccess;
 }
 
 // grid = number of SMs (one CTA per SM: A buffers + rings take ~210 KB of shared memory)
 void launch_k1_tcp(const Dev& D, int grid, cudaStream_t st, int cur) {
-  if (D.R <= 1) launch_r<1>(D, grid, st, cur);
-  else if (D.R <= 2) launch_r<2>(D, grid, st, cur);
-  else if (D.R <= 4) launch_r<4>(D, grid, st, cur);
-  else if (D.R <= 8) launch_r<8>(D, grid, st, cur);
-  else launch_r<16>(D, grid, st, cur);
+  if (D.storage == 1) launch_st<1>(D, grid, st, cur);
+  else launch_st<2>(D, grid, st, cur);
 }

@@ -257,3 +257,30 @@ def test_tc2_several_tiles_per_cta_equals_simt(cuda_ok, taus):
         del S
     for u, v in zip(out[0], out[1]):
         np.testing.assert_array_equal(u, v)
+
+
+@pytest.mark.parametrize("n,p,taus,esmax", [(1500, 2600, [0.5], 65536), (999, 3100, [0.3, 0.7], 65536),
+                                            (4097, 1800, [0.2, 0.5, 0.8], 65536),
+                                            (2500, 2000, [0.1 * k for k in range(1, 10)], 65536),
+                                            (700, 1500, [k / 17 for k in range(1, 17)], 65536),
+                                            (1100, 3000, [0.5], 64)])
+def test_k1_tcu_u8_equals_cuda_core_forward(cuda_ok, monkeypatch, n, p, taus, esmax):
+    """The tensor-core forward product for u8 storage (k1_tcp<., 1>: cp.async straight into the
+    swizzled A tile) forms the same exact sums as the CUDA-core k1_bulk, 1-16 RHS, ragged slabs,
+    and many work items per CTA."""
+    import paper_2601_02826_b200 as fs
+
+    b = datagen.make("c5", n=n, p=p, storage=fs.U8)
+    X, y = to_device(b)
+    eta = [40.0] * 5
+    lams = [0.02 if esmax == 65536 else 0.0] * len(taus)
+    out = []
+    for mode in ("bulk", "tcu"):
+        monkeypatch.setenv("FSQR_K1", mode)
+        monkeypatch.setenv("FSQR_K1_ESMAX", str(esmax))
+        S = fs.Solver(X, fs.U8, b.n, b.p, b.ld, y, taus, lams, G=5, eta=eta)
+        S.iterate(40)
+        out.append(S.state() + (S.objective(),))
+        del S
+    for u, v in zip(out[0], out[1]):
+        np.testing.assert_array_equal(u, v)
