@@ -255,7 +255,9 @@ def run_ours(args):
     stage_ms, prof_total_ms = fs.fsqr_profile_iterate(S.ctx, args.steps)
 
     # roofline of the dominant kernel (K2: X~^T theta + beta prox), algorithmic bytes per launch
-    xbytes = prob.n * prob.p // (4 if pack else 1)  # every genotype code (1 byte, or 2 bits packed), read once
+    two_bit = pack or prob.storage == fs.PACKED2
+    # every stored element read once: 2-bit codes, u8 codes, or fp32 values (C1)
+    xbytes = prob.n * prob.p // 4 if two_bit else prob.n * prob.p * (4 if prob.storage == fs.F32_DENSE else 1)
     state_bytes = 28 * prob.p                       # beta r/w (16 B) + colsum (4 B) + 1/s_j (8 B) per column
     k2_ms = stage_ms[0] / k
     peak, peak_kind = peaks()
@@ -263,7 +265,7 @@ def run_ours(args):
     traffic = k2_traffic(args.config + ("_pack2" if pack else ""))
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic,
-            "kernel": ("k2_tc2_kernel<16,1>" if pack else "k2_tc_kernel<16,1>") if S.backend == "tc" else "k2_simt", "peak_source": peak_kind,
+            "kernel": ("k2_tc2_kernel<16,1>" if two_bit else "k2_tc_kernel<16,1>") if S.backend == "tc" else "k2_simt", "peak_source": peak_kind,
             "algorithmic_bytes_per_launch": xbytes + state_bytes,
             "kernel_share_of_step": stage_ms[0] / prof_total_ms}
 
@@ -346,12 +348,17 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": ws, "steps": k, "warmup": args.warmup,
             "ms_per_step": total_ms / k, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": ("u2" if pack else "u8") + "xs8->s32 exact, f64", "data": "synthetic",
-            "config": {"workload": "C5 design/response, single RHS tau=0.5 (BASELINE metric)", "n": prob.n,
-                       "p": prob.p, "storage": "u8 input" + (", repacked to 2 bits at create (FSQR_DESIGN_PACK2)"
-                                                             if pack else ", streamed as u8"), "tau": tau, "lambda": prob.lam_frac * lm, "lambda_frac":
+            "dtype": ("f64" if prob.storage == fs.F32_DENSE else ("u2" if two_bit else "u8") + "xs8->s32 exact, f64"),
+            "data": "synthetic",
+            "config": {"workload": ("C5 design/response, single RHS tau=0.5 (BASELINE metric)" if args.config == "m"
+                                    else f"config {args.config}, first tau only (not the metric workload)"), "n": prob.n,
+                       "p": prob.p, "storage": {fs.U8: "u8 input", fs.PACKED2: "2-bit packed", fs.F32_DENSE: "fp32"}[prob.storage]
+                       + (", repacked to 2 bits at create (FSQR_DESIGN_PACK2)" if pack else
+                          (", streamed as u8" if prob.storage == fs.U8 else "")), "tau": tau, "lambda": prob.lam_frac * lm, "lambda_frac":
                        prob.lam_frac, "G": G, "mu": mu, "burn_in": args.burn_in, "support": nnz,
-                       "l2": f"X ({xbytes / 1e9:.1f} GB streamed) >> L2 (126 MB): no flush needed", "parallelism": f"replicas x{ws}",
+                       "l2": (f"X ({xbytes / 1e9:.1f} GB streamed) >> L2 (126 MB): no flush needed" if xbytes > 126e6
+                              else f"X ({xbytes / 1e6:.0f} MB) fits in L2: not flushed (not the metric workload)"),
+                       "parallelism": f"replicas x{ws}",
                        "backend": S.backend, "setup_s": t_setup, "datagen_s": t_gen},
             "u8_storage": u8_line,
             "x_stream_gbs": xbytes / (total_ms / k / 1000.0) / 1e9,
