@@ -345,7 +345,15 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize_mc(const Dev D) {
         t2 = block_sum_ll(t2, smll);
         if (threadIdx.x == 0) D.Tsum[r] = t2;
       }
+      if (D.R == 1) {   // one RHS: its last CTA is the last CTA overall, no second ticket round
+        if (threadIdx.x == 0) {
+          D.cmax[par] = 0ull;
+          D.sup_cnt[par] = 0;
+          *D.iter = k + 1;
+        }
+      }
     }
+    if (D.R == 1) return;
   }
   // ------------------------------------------------ last CTA overall: iteration tail
   __threadfence();
