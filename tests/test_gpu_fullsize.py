@@ -181,7 +181,7 @@ def test_m_full_trajectory(cuda_ok, pack):
 
 # ------------------------------------------------------------------ one-step properties at full size
 
-@pytest.mark.parametrize("name", ["m", "m_pack2", "c3", "c4", "c5"])
+@pytest.mark.parametrize("name", ["m", "m_pack2", "c3", "c4", "c5", "c5_pack2"])
 def test_full_size_step_properties(cuda_ok, name):
     import paper_2601_02826_b200 as fs
 
