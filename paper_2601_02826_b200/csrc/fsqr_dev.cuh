@@ -132,6 +132,12 @@ __device__ __forceinline__ double prox_beta(double b, double g, double lam, doub
   return (pos_part(a - lam) - pos_part(-a - lam)) / eta;
 }
 
+// E14 with a precomputed 1/eta (the product differs from the quotient by at most one rounding)
+__device__ __forceinline__ double prox_beta_inv(double b, double g, double lam, double eta, double inv_eta) {
+  double a = eta * b + g;
+  return (pos_part(a - lam) - pos_part(-a - lam)) * inv_eta;
+}
+
 // soft-threshold S_c(v) for the KKT residual
 __device__ __forceinline__ double soft_thr(double v, double c) {
   return v > c ? v - c : (v < -c ? v + c : 0.0);
@@ -383,6 +389,7 @@ __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, i
   const int64_t j = c + 1;
   const double isd = valid ? D.inv_sd[c] : 0.0;
   const double eta = valid ? D.eta[block_of_col(D, j)] : 1.0;
+  const double inv_eta = 1.0 / eta;   // one division per column, shared by every RHS
   bool nz = false;
 #pragma unroll
   for (int r = 0; r < RMAX; ++r) {
@@ -404,7 +411,7 @@ __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, i
       x[4] = (b != 0.0) ? 1.0 : 0.0;
       if (D.update) {
         // E14, or the elastic-net block prox (Remark 3, L347-349; reading R19) when lam2 > 0
-        const double bn = l2 == 0.0 ? prox_beta(b, g[r], lam, eta)
+        const double bn = l2 == 0.0 ? prox_beta_inv(b, g[r], lam, eta, inv_eta)
                                     : (pos_part(eta * b + g[r] - lam) - pos_part(-eta * b - g[r] - lam)) / (eta + l2);
         C.beta_out[j * C.R + r] = bn;
         if (bn != 0.0) {
