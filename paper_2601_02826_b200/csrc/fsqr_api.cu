@@ -78,7 +78,7 @@ struct fsqr_ctx {
   std::vector<void*> allocs;
   std::string err;
   fsqr_options opt{};
-  std::vector<double> tau, lambda, lambda_max, eta;
+  std::vector<double> tau, lambda, lambda_max, eta, inv_eta;
   int R = 1, T = 0;
   int64_t n = 0, p = 0;
   double* h_pin = nullptr;  // small pinned scratch
@@ -546,12 +546,13 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
 
   // ---------------- allocations
   int32_t* colsum;
-  double *mean, *inv_sd, *sd, *eta_d, *y, *tau_d, *lam_cur;
+  double *mean, *inv_sd, *sd, *eta_d, *inv_eta_d, *y, *tau_d, *lam_cur;
   AL(colsum, X->p);
   AL(mean, X->p);
   AL(inv_sd, X->p);
   AL(sd, X->p);
   AL(eta_d, o.G);
+  AL(inv_eta_d, o.G);
   AL(y, X->n);
   AL(tau_d, R);
   AL(lam_cur, R);
@@ -559,6 +560,7 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
   D.mean = mean;
   D.inv_sd = inv_sd;
   D.eta = eta_d;
+  D.inv_eta = inv_eta_d;
   D.y = y;
   D.tau = tau_d;
   D.lam_cur = lam_cur;
@@ -666,6 +668,9 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
     if (s != FSQR_OK) return s;
   }
   CK(cudaMemcpyAsync(eta_d, ctx->eta.data(), sizeof(double) * o.G, cudaMemcpyHostToDevice, st));
+  ctx->inv_eta.resize(o.G);
+  for (int g = 0; g < o.G; ++g) ctx->inv_eta[g] = 1.0 / ctx->eta[g];
+  CK(cudaMemcpyAsync(inv_eta_d, ctx->inv_eta.data(), sizeof(double) * o.G, cudaMemcpyHostToDevice, st));
 
   // ---------------- lambda_max per tau
   {

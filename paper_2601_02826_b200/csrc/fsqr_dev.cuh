@@ -48,6 +48,7 @@ struct Dev {
   double* lamw;                     // [(p+1)*R] penalty weights w_jr (lam_jr = lam_r w_jr), coefficient-major
   int* use_w;                       // [1] device flag: 0 -> all weights 1 (lamw not read)
   const double* eta;                // [G]
+  const double* inv_eta;            // [G] 1/eta_g (host IEEE division; E14 multiplies by it)
   // state
   double* beta[2];                  // [(p+1)*R], coefficient-major
   double* z;                        // [R*n]
@@ -120,8 +121,9 @@ __device__ __forceinline__ int bq_index(const Dev& D, int i) {
 
 __device__ __forceinline__ int block_of_col(const Dev& D, int64_t j) {
   // contiguous near-equal blocks of the p+1 model columns (first `grem` blocks hold q+1)
-  int64_t big = D.grem * (D.gq + 1);
-  return (int)(j < big ? j / (D.gq + 1) : D.grem + (j - big) / D.gq);
+  // p + 1 <= 2^31, so 32-bit unsigned divisions suffice (a 64-bit one is a long software sequence)
+  const uint32_t q1 = (uint32_t)(D.gq + 1), big = (uint32_t)(D.grem * (D.gq + 1)), jj = (uint32_t)j;
+  return (int)(jj < big ? jj / q1 : (uint32_t)D.grem + (jj - big) / (uint32_t)D.gq);
 }
 
 __device__ __forceinline__ double pos_part(double v) { return v > 0.0 ? v : 0.0; }
@@ -388,8 +390,9 @@ __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, i
                                            K2Part<RMAX>& P, double* cval, double* bval, bool valid = true) {
   const int64_t j = c + 1;
   const double isd = valid ? D.inv_sd[c] : 0.0;
-  const double eta = valid ? D.eta[block_of_col(D, j)] : 1.0;
-  const double inv_eta = 1.0 / eta;   // one division per column, shared by every RHS
+  const int gb = valid ? block_of_col(D, j) : 0;
+  const double eta = valid ? D.eta[gb] : 1.0;
+  const double inv_eta = valid ? D.inv_eta[gb] : 1.0;   // E14 multiplies by 1/eta_g
   bool nz = false;
 #pragma unroll
   for (int r = 0; r < RMAX; ++r) {
