@@ -35,6 +35,9 @@
 #ifndef K1P_SMEM_KB
 #define K1P_SMEM_KB 220
 #endif
+#ifndef K1P_NAB2
+#define K1P_NAB2 2     // A tile buffers of the 2-bit variant (measurement knob)
+#endif
 #ifndef K1P_CTAS
 #define K1P_CTAS 1     // CTAs per SM the launch grid assumes
 #endif
@@ -61,7 +64,7 @@ struct K1P {
   static constexpr int UPL = ST == 1 ? RT : RT / 4;            // 16-byte units per lane per chunk
   static constexpr int DSTAGE = ST == 1 ? 0 : KC * SEGB;       // one chunk of packed segments (2-bit)
   static constexpr int BTILE = N * KC;
-  static constexpr int NAB = ST == 1 ? 3 : 2;                  // A tile buffers (u8: the copy ring)
+  static constexpr int NAB = ST == 1 ? 3 : K1P_NAB2;           // A tile buffers (u8: the copy ring)
   static constexpr int ABUF = RT * ATILE;
   static constexpr int MB = RMAX <= 4 ? 256 : 128;             // metadata entries per block
   static constexpr int META = 2 * MB * (4 + 8 * RMAX);         // two blocks: colsum, beta/s
