@@ -25,6 +25,9 @@
  *  - beta is stored coefficient-major: beta[j*n_rhs + r], j = 0..p.
  *  - Streams: `stream` is a cudaStream_t (CUstream) handle passed as void*;
  *    NULL means the legacy default stream.  All work is enqueued on it.
+ *    Calls that take no stream (fsqr_set_lambda, fsqr_set_lambda2, fsqr_get_colstats,
+ *    fsqr_path_hbic, fsqr_path_beta, fsqr_trace, fsqr_iterations) first wait for the whole
+ *    device, so they never race with iterations still queued on a caller's stream.
  *  - No call aborts or prints.  Failures return a status < 0 and the message
  *    is available from fsqr_last_error(ctx) (or fsqr_global_error() when no
  *    context exists).  FSQR_NOT_CONVERGED is a flag, not an error: the state
@@ -216,10 +219,13 @@ fsqr_status fsqr_get_colstats(fsqr_ctx* ctx, double* mean_host, double* sd_host)
 /*
  * Warm-started lambda path: RHS r walks lam_path_host[r*T + t],
  * t = 0..T-1, all RHS in lockstep through one pass over X per iteration.  When R(w^k) <= tol at
- * point t (or max_iter_point iterations were spent there) w^k is recorded as point t and RHS r moves
- * to lam_{t+1} from the next iteration; after its last point it is frozen.  Blocking.
- * iters_host [n_rhs][T], obj_host [n_rhs][T], R_host [n_rhs][T][3], nnz_host [n_rhs][T],
- * converged_host [n_rhs][T] (any may be NULL).  Returns the lockstep iteration count in *total.
+ * point t (or max_iter_point updates were taken there) w^k is recorded as point t and is itself the
+ * initialisation of point t+1 ("the solution from the preceding lambda serves as the
+ * initialization", L412; reading R10): the update that pass computed with lam_t is
+ * discarded and the next pass re-tests w^k at lam_{t+1}.  After its last point the RHS is frozen.
+ * Blocking.  iters_host [n_rhs][T] (updates taken at each point), obj_host [n_rhs][T],
+ * R_host [n_rhs][T][3], nnz_host [n_rhs][T], converged_host [n_rhs][T] (any may be NULL).
+ * *total = lockstep passes over X (updates plus the T-1 re-tests per RHS that share them).
  */
 fsqr_status fsqr_path(fsqr_ctx* ctx, const double* lam_path_host, int32_t T, int64_t* total, int64_t* iters_host,
                       double* obj_host, double* R_host, int64_t* nnz_host, int32_t* converged_host, void* stream);
@@ -229,8 +235,10 @@ fsqr_status fsqr_path(fsqr_ctx* ctx, const double* lam_path_host, int32_t T, int
  * settings, L406-411).  FSQR_ERR_STATE before fsqr_path. */
 fsqr_status fsqr_path_hbic(fsqr_ctx* ctx, double* hbic_host);
 
-/* Sparse solution of path point t for RHS r: writes up to cap (index j, beta_j standardised) pairs,
- * returns the count in *count (which may exceed cap: then only cap were written). */
+/* Sparse solution of path point t for RHS r: writes up to cap (index j, beta_j standardised) pairs
+ * in ascending j (deterministic), returns the count of nonzeros in *count (which may exceed cap:
+ * then only cap were written).  The store keeps min(p+1, 4n+64) entries per point: a point with
+ * more nonzeros returns FSQR_ERR_STATE (after writing the first ones) instead of truncating silently. */
 fsqr_status fsqr_path_beta(fsqr_ctx* ctx, int32_t r, int32_t t, int64_t cap, int64_t* idx_host, double* beta_host,
                            int64_t* count);
 

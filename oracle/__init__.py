@@ -46,8 +46,10 @@ _lib = None
 def build(force: bool = False) -> str:
     """Compile the oracle (plain C, IEEE fp64, no fast-math, no FMA contraction)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = f"{_LIB}.{os.getpid()}.tmp"   # build aside, then rename: a running process keeps its copy
         subprocess.check_call(["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
-                               "-shared", "-o", _LIB, _SRC, "-lm"])
+                               "-shared", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
     return _LIB
 
 

@@ -454,14 +454,15 @@ int orc_solve(const orc_design* X, const double* y, const orc_opts* o, double* b
 }
 
 /*
- * Warm-started lambda path for one tau.
- * lam_t = lam_path[t] * w_j (w_0 = 0).  The iterate w^k that first satisfies
- * R(w^k) <= tol at lam_t (or reaches max_iter_point iterations at that point)
- * is recorded as point t; the update of that same iteration k is still taken
- * with lam_t, and iteration k+1 onward uses lam_{t+1} (the GPU state machine
- * switches lambda between the check and the next X~^T theta pass).
- * Outputs per point: iters[t] (iterations spent at the point), R_out[3t..],
- * obj[t], beta_path[t*(p+1)..] (dense, optional).  Returns total iterations.
+ * Warm-started lambda path for one tau ("the solution from the preceding lambda
+ * serves as the initialization").  For t = 0..T-1 with
+ * lam_t = lam_path[t] * w_j (w_0 = 0), Algorithm 1 runs from the current (beta, z, theta):
+ *   g = X~^T theta^k, R(w^k) at lam_t;
+ *   if R(w^k) <= tol, or max_iter_point updates were taken at this point: w^k is point t, and
+ *     the same w^k is the initialisation of point t+1 (tested again there, at lam_{t+1});
+ *   else one update with lam_t (E14, E15, L287, E12).
+ * Outputs per point: iters[t] (updates taken at the point), R_out[3t..], obj[t],
+ * beta_path[t*(p+1)..] (dense, optional), converged[t].  Returns the total number of updates.
  */
 int64_t orc_path(const orc_design* X, const double* y, double tau, double mu, int32_t G, const double* eta,
                  const double* w, const double* lam_path, int32_t T, double tol, int64_t max_iter_point,
@@ -478,42 +479,36 @@ int64_t orc_path(const orc_design* X, const double* y, double tau, double mu, in
   double* r = (double*)malloc(sizeof(double) * n);
   orc_fwdprod(X, beta, s);
   for (int64_t i = 0; i < n; ++i) r[i] = s[i] + z[i] - y[i];
-  int32_t t = 0;
-  for (int64_t j = 0; j < p1; ++j) lam[j] = lam_path[0] * w[j];
-  int64_t k = 0, kpt = 0;
-  for (;; ++k) {
-    orc_backprod(X, theta, g);
-    double Rk[3];
-    kkt_parts(n, p1, y, tau, lam, 0.0, beta, z, theta, g, s, Rk);
-    double Rmax = fmax(Rk[0], fmax(Rk[1], Rk[2]));
-    int switch_now = 0;
-    if (Rmax <= tol || kpt == max_iter_point) {
-      double loss = 0.0, pen = 0.0;
-      for (int64_t i = 0; i < n; ++i) loss += orc_rho(y[i] - s[i], tau);
-      for (int64_t j = 1; j < p1; ++j) pen += lam[j] * fabs(beta[j]);
-      iters[t] = kpt;
-      R_out[3 * t] = Rk[0];
-      R_out[3 * t + 1] = Rk[1];
-      R_out[3 * t + 2] = Rk[2];
-      obj[t] = loss / (double)n + pen;
-      converged[t] = Rmax <= tol;
-      if (beta_path) memcpy(beta_path + (int64_t)t * p1, beta, sizeof(double) * p1);
-      if (t == T - 1) break;
-      switch_now = 1;
-    }
-    for (int64_t j = 0; j < p1; ++j) beta[j] = orc_prox_beta(beta[j], g[j], lam[j], eta[blk[j]]);
-    for (int64_t i = 0; i < n; ++i) z[i] = orc_prox_z(z[i], theta[i], mu, tau, n);
-    orc_fwdprod(X, beta, s);
-    for (int64_t i = 0; i < n; ++i) {
-      double rn = s[i] + z[i] - y[i];
-      theta[i] = orc_dual(theta[i], rn, r[i], mu, G);
-      r[i] = rn;
-    }
-    ++kpt;
-    if (switch_now) {
-      ++t;
-      kpt = 0;
-      for (int64_t j = 0; j < p1; ++j) lam[j] = lam_path[t] * w[j];
+  int64_t total = 0;
+  for (int32_t t = 0; t < T; ++t) {
+    for (int64_t j = 0; j < p1; ++j) lam[j] = lam_path[t] * w[j];
+    for (int64_t kpt = 0;; ++kpt) {
+      orc_backprod(X, theta, g);
+      double Rk[3];
+      kkt_parts(n, p1, y, tau, lam, 0.0, beta, z, theta, g, s, Rk);
+      double Rmax = fmax(Rk[0], fmax(Rk[1], Rk[2]));
+      if (Rmax <= tol || kpt == max_iter_point) {
+        double loss = 0.0, pen = 0.0;
+        for (int64_t i = 0; i < n; ++i) loss += orc_rho(y[i] - s[i], tau);
+        for (int64_t j = 1; j < p1; ++j) pen += lam[j] * fabs(beta[j]);
+        iters[t] = kpt;
+        R_out[3 * t] = Rk[0];
+        R_out[3 * t + 1] = Rk[1];
+        R_out[3 * t + 2] = Rk[2];
+        obj[t] = loss / (double)n + pen;
+        converged[t] = Rmax <= tol;
+        if (beta_path) memcpy(beta_path + (int64_t)t * p1, beta, sizeof(double) * p1);
+        break;
+      }
+      for (int64_t j = 0; j < p1; ++j) beta[j] = orc_prox_beta(beta[j], g[j], lam[j], eta[blk[j]]);
+      for (int64_t i = 0; i < n; ++i) z[i] = orc_prox_z(z[i], theta[i], mu, tau, n);
+      orc_fwdprod(X, beta, s);
+      for (int64_t i = 0; i < n; ++i) {
+        double rn = s[i] + z[i] - y[i];
+        theta[i] = orc_dual(theta[i], rn, r[i], mu, G);
+        r[i] = rn;
+      }
+      ++total;
     }
   }
   free(start);
@@ -522,7 +517,7 @@ int64_t orc_path(const orc_design* X, const double* y, double tau, double mu, in
   free(g);
   free(s);
   free(r);
-  return k;
+  return total;
 }
 
 /* ------------------------------------------------ folded-concave penalties (Section 5) */

@@ -55,3 +55,22 @@ def highs(A: np.ndarray, y: np.ndarray, tau: float, lam: np.ndarray):
     res = linprog(c, A_eq=Aeq, b_eq=y, bounds=bounds, method="highs")
     beta = np.concatenate([[res.x[0]], res.x[1:1 + p] - res.x[1 + p:1 + 2 * p]])
     return float(res.fun), beta
+
+
+def highs_saddle(A: np.ndarray, y: np.ndarray, tau: float, lam: np.ndarray):
+    """The LP above with its equality duals: (beta*, z* = u - v = y - A beta*, theta*) where theta* are the
+    marginals of y - A beta = u - v.  LP duality gives theta* in [(tau-1)/n, tau/n] (u, v columns),
+    sum theta* = 0 (free beta_0) and |A_j^T theta*| <= lam_j (a_j, b_j columns) with complementary
+    slackness: exactly the saddle-point conditions of Prop. 1."""
+    from scipy.optimize import linprog
+
+    n, d = A.shape
+    p = d - 1
+    c = np.concatenate([[0.0], lam[1:], lam[1:], np.full(n, tau / n), np.full(n, (1.0 - tau) / n)])
+    Aeq = np.hstack([A[:, :1], A[:, 1:], -A[:, 1:], np.eye(n), -np.eye(n)])
+    bounds = [(None, None)] + [(0, None)] * (2 * p + 2 * n)
+    res = linprog(c, A_eq=Aeq, b_eq=y, bounds=bounds, method="highs-ds",
+                  options=dict(primal_feasibility_tolerance=1e-10, dual_feasibility_tolerance=1e-10))
+    beta = np.concatenate([[res.x[0]], res.x[1:1 + p] - res.x[1 + p:1 + 2 * p]])
+    z = res.x[1 + 2 * p:1 + 2 * p + n] - res.x[1 + 2 * p + n:]   # u - v: exact zeros on the interpolated rows
+    return beta, z, np.asarray(res.eqlin.marginals, np.float64)

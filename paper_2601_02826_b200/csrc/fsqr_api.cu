@@ -73,8 +73,9 @@ struct fsqr_ctx {
   int sms = 148;
   int k2_grid = 148, k1_grid = 148;
   int chunk = 16;
-  CUtensorMap tmX{}, tmB{}, tmG{};
+  CUtensorMap tmX{}, tmB{};
   cudaStream_t cap_stream = nullptr;
+  cudaStream_t alloc_st = nullptr;   // stream of the API call that is allocating (zero-fill is ordered on it)
   std::vector<void*> allocs;
   std::string err;
   fsqr_options opt{};
@@ -121,12 +122,18 @@ fsqr_status dalloc(fsqr_ctx* ctx, T** p, size_t count) {
   if (count == 0) count = 1;
   cudaError_t e = cudaMalloc(&q, count * sizeof(T));
   if (e != cudaSuccess) return set_err(ctx, FSQR_ERR_OOM, "cudaMalloc(%zu bytes): %s", count * sizeof(T), cudaGetErrorString(e));
-  e = cudaMemset(q, 0, count * sizeof(T));
-  if (e != cudaSuccess) return set_err(ctx, FSQR_ERR_CUDA, "cudaMemset: %s", cudaGetErrorString(e));
+  // zero-fill on the calling API's stream: a legacy-stream cudaMemset is not ordered against the
+  // caller's (typically non-blocking) stream and could land after work enqueued there
+  e = cudaMemsetAsync(q, 0, count * sizeof(T), ctx->alloc_st);
+  if (e != cudaSuccess) return set_err(ctx, FSQR_ERR_CUDA, "cudaMemsetAsync: %s", cudaGetErrorString(e));
   ctx->allocs.push_back(q);
   *p = (T*)q;
   return FSQR_OK;
 }
+
+// calls without a stream argument read or write state that queued work may still be using: they
+// first wait for the device (a legacy-stream cudaMemcpy is not ordered against non-blocking streams)
+#define SYNC_DEVICE() CK(cudaDeviceSynchronize())
 
 #define AL(ptr, cnt)                                        \
   do {                                                      \
@@ -170,18 +177,6 @@ fsqr_status make_tmaps(fsqr_ctx* ctx) {
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_err(ctx, FSQR_ERR_CUDA, "tensor map for theta digits failed (%d)", (int)r);
-  }
-  if (D.k1_tc == 2) {
-    // forward gather: 128-row windows of single columns, four columns per tile::gather4
-    cuuint64_t dims[2] = {(cuuint64_t)D.ld, (cuuint64_t)D.p};
-    cuuint64_t strides[1] = {(cuuint64_t)D.ld};
-    cuuint32_t box[2] = {128, 1};
-    cuuint32_t es[2] = {1, 1};
-    CUresult r = enc(&ctx->tmG, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)D.X8, dims, strides, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return set_err(ctx, FSQR_ERR_CUDA, "tensor map for the forward gather failed (%d)", (int)r);
-    ctx->D.tmG = &ctx->tmG;
   }
   return FSQR_OK;
 }
@@ -405,6 +400,7 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
                                const double* tau, const double* lambda, const double* lamw_dev,
                                const fsqr_options* opt, cudaStream_t st) {
   // ---------------- validation
+  ctx->alloc_st = st;
   if (!X || !y_dev || !tau || !lambda) return set_err(ctx, FSQR_ERR_CONFIG, "null argument");
   if (R < 1 || R > FSQR_MAXR) return set_err(ctx, FSQR_ERR_CONFIG, "n_rhs=%d not in [1,%d]", R, FSQR_MAXR);
   if (X->storage < 0 || X->storage > 2) return set_err(ctx, FSQR_ERR_CONFIG, "bad storage %d", X->storage);
@@ -520,28 +516,17 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
   } else {
     ctx->k2_grid = ctx->sms * 8;
   }
-  ctx->k1_grid = ctx->sms;   // k1_bulk scales by its resident CTAs per SM; k1_tc runs one CTA per SM
+  ctx->k1_grid = ctx->sms;   // k1_bulk scales by its resident CTAs per SM; k1_tcp runs one CTA per SM
   CK(k1_init());
-  // forward-product kernel.  History: with 3+ RHS the CUDA-core k1_bulk's 2R multiply-adds per
-  // element lost to the gather4 tensor-core kernel (C5 at 0.05 lambda_max: 0.80 vs 2.43 ms), whose
-  // one TMA operation per 512 bytes made it the slower one for 1-2 RHS (M: 140 vs 55 us).
-  // FSQR_K1=bulk|tc|gather|tcp|tcu overrides, for measurements.
-  // k1_tcp (tensor cores, A tile built on chip from per-lane cp.async) beats both for genotype
-  // storage: 2-bit M 53 -> 29 us and C4 210 -> 104 us (in-place code planes); u8 M 59 -> 54 us,
-  // C2 3 RHS 31 -> 14 us, C5 9 RHS 18.5 -> 14.4 us against the gather kernel.
+  // forward-product kernel: k1_tcp (tensor cores, A tile built on chip from per-lane cp.async) for
+  // genotype storage -- 2-bit M 53 -> 29 us and C4 210 -> 104 us against the CUDA-core k1_bulk,
+  // u8 C2 3 RHS 31 -> 14 us and C5 9 RHS 18.5 -> 14.4 us against a TMA gather4 kernel (round 1,
+  // since removed).  FSQR_K1=bulk selects k1_bulk (the bitwise cross-check of the tests).
   D.k1_tc = 0;
   if (ctx->backend == FSQR_BACKEND_TC && X->storage == FSQR_U8) D.k1_tc = 4;
   if (ctx->backend == FSQR_BACKEND_TC && X->storage == FSQR_PACKED2) D.k1_tc = 3;
-  if (const char* ev = getenv("FSQR_K1")) {
+  if (const char* ev = getenv("FSQR_K1"))
     if (!strcmp(ev, "bulk")) D.k1_tc = 0;
-    else if (!strcmp(ev, "tc") && X->storage != FSQR_F32_DENSE) D.k1_tc = 1;
-    else if (!strcmp(ev, "gather") && X->storage == FSQR_U8) D.k1_tc = 2;
-    else if (!strcmp(ev, "tcp") && X->storage == FSQR_PACKED2) D.k1_tc = 3;
-    else if (!strcmp(ev, "tcu") && X->storage == FSQR_U8) D.k1_tc = 4;
-
-  }
-  if (D.k1_tc == 1) CK(k1_tc_init());
-  if (D.k1_tc == 2) CK(k1_tcg_init());
   if (D.k1_tc == 3 || D.k1_tc == 4) CK(k1_tcp_init());
 
   // ---------------- allocations
@@ -868,6 +853,7 @@ fsqr_status fsqr_set_lambda_weights(fsqr_ctx* ctx, const double* w_host, void* s
 
 fsqr_status fsqr_set_lambda2(fsqr_ctx* ctx, const double* lam2_host) {
   if (!ctx || !lam2_host) return set_err(ctx, FSQR_ERR_CONFIG, "null argument");
+  SYNC_DEVICE();
   for (int r = 0; r < ctx->R; ++r)
     if (!(lam2_host[r] >= 0.0) || !std::isfinite(lam2_host[r]))
       return set_err(ctx, FSQR_ERR_CONFIG, "lambda2[%d]=%g invalid", r, lam2_host[r]);
@@ -912,6 +898,7 @@ fsqr_status fsqr_pivotal(fsqr_ctx* ctx, int32_t rhs, int64_t B, uint64_t seed, d
   cudaStream_t st = (cudaStream_t)stream;
   const int ldk = (int)(((ctx->n + 127) / 128) * 128);
   const bool packed = ctx->D.storage == FSQR_PACKED2;
+  ctx->alloc_st = st;
   if (!ctx->piv_draws) {
     AL(ctx->piv_draws, (size_t)128 * ldk);
     AL(ctx->piv_nb, 128);
@@ -1047,19 +1034,24 @@ fsqr_status fsqr_set_state(fsqr_ctx* ctx, const double* beta_host, const double*
       if (!std::isfinite(b)) return set_err(ctx, FSQR_ERR_DATA, "beta not finite");
       bt[(size_t)j * R + r] = b;
     }
-  CK(cudaStreamSynchronize(st));
-  CK(cudaMemcpy(ctx->D.beta[0], bt.data(), sizeof(double) * bt.size(), cudaMemcpyHostToDevice));
+  const size_t nR0 = (size_t)R * ctx->n;
+  for (size_t i = 0; i < nR0; ++i)
+    if (!std::isfinite(z_host[i]) || !std::isfinite(theta_host[i]))
+      return set_err(ctx, FSQR_ERR_DATA, "z or theta not finite at %zu", i);
+  // everything on the caller's stream, in order after any work still queued there
+  CK(cudaMemcpyAsync(ctx->D.beta[0], bt.data(), sizeof(double) * bt.size(), cudaMemcpyHostToDevice, st));
   const size_t nR = (size_t)R * ctx->n;
-  CK(cudaMemcpy(ctx->D.z, z_host, sizeof(double) * nR, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(ctx->D.theta, theta_host, sizeof(double) * nR, cudaMemcpyHostToDevice));
-  CK(cudaMemset(ctx->D.iter, 0, sizeof(long long)));
-  CK(cudaMemset(ctx->D.status, 0, sizeof(int) * R));
-  CK(cudaMemset(ctx->D.commit_iter, 0, sizeof(long long) * R));
-  return init_state(ctx, st);
+  CK(cudaMemcpyAsync(ctx->D.z, z_host, sizeof(double) * nR, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ctx->D.theta, theta_host, sizeof(double) * nR, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(ctx->D.iter, 0, sizeof(long long), st));
+  CK(cudaMemsetAsync(ctx->D.status, 0, sizeof(int) * R, st));
+  CK(cudaMemsetAsync(ctx->D.commit_iter, 0, sizeof(long long) * R, st));
+  return init_state(ctx, st);   // synchronises st before bt goes out of scope
 }
 
 fsqr_status fsqr_set_lambda(fsqr_ctx* ctx, const double* lambda_host) {
   if (!ctx || !lambda_host) return set_err(ctx, FSQR_ERR_CONFIG, "null argument");
+  SYNC_DEVICE();
   for (int r = 0; r < ctx->R; ++r)
     if (!(lambda_host[r] >= 0.0) || !std::isfinite(lambda_host[r]))
       return set_err(ctx, FSQR_ERR_CONFIG, "lambda[%d] invalid", r);
@@ -1082,6 +1074,7 @@ fsqr_status fsqr_get_eta(const fsqr_ctx* ctx, double* eta_host) {
 
 fsqr_status fsqr_get_colstats(fsqr_ctx* ctx, double* mean_host, double* sd_host) {
   if (!ctx) return set_err(nullptr, FSQR_ERR_CONFIG, "ctx is NULL");
+  SYNC_DEVICE();
   if (mean_host) CK(cudaMemcpy(mean_host, ctx->D.mean, sizeof(double) * ctx->p, cudaMemcpyDeviceToHost));
   if (sd_host) {
     std::vector<double> isd(ctx->p);
@@ -1099,6 +1092,7 @@ fsqr_status fsqr_path(fsqr_ctx* ctx, const double* lam_path_host, int32_t T, int
   for (int64_t q = 0; q < (int64_t)R * T; ++q)
     if (!(lam_path_host[q] >= 0.0)) return set_err(ctx, FSQR_ERR_CONFIG, "lam_path[%lld] invalid", (long long)q);
   Dev& D = ctx->D;
+  ctx->alloc_st = st;
   if (T != ctx->T || !D.path_rec) {
     ctx->T = T;
     ctx->path_cap = std::min<int64_t>(ctx->p + 1, 4 * ctx->n + 64);
@@ -1159,6 +1153,7 @@ fsqr_status fsqr_path(fsqr_ctx* ctx, const double* lam_path_host, int32_t T, int
 
 fsqr_status fsqr_path_hbic(fsqr_ctx* ctx, double* hbic_host) {
   if (!ctx || !hbic_host) return set_err(ctx, FSQR_ERR_CONFIG, "null argument");
+  SYNC_DEVICE();
   if (!ctx->D.path_rec) return set_err(ctx, FSQR_ERR_STATE, "fsqr_path has not run");
   const int R = ctx->R, T = ctx->T;
   std::vector<double> rec((size_t)R * T * FSQR_PATH_W);
@@ -1174,6 +1169,7 @@ fsqr_status fsqr_path_hbic(fsqr_ctx* ctx, double* hbic_host) {
 fsqr_status fsqr_path_beta(fsqr_ctx* ctx, int32_t r, int32_t t, int64_t cap, int64_t* idx_host, double* beta_host,
                            int64_t* count) {
   if (!ctx || !count) return set_err(ctx, FSQR_ERR_CONFIG, "null argument");
+  SYNC_DEVICE();
   if (!ctx->D.path_rec) return set_err(ctx, FSQR_ERR_STATE, "fsqr_path has not run");
   if (r < 0 || r >= ctx->R || t < 0 || t >= ctx->T) return set_err(ctx, FSQR_ERR_CONFIG, "bad (r, t)");
   const size_t q = (size_t)r * ctx->T + t;
@@ -1187,11 +1183,17 @@ fsqr_status fsqr_path_beta(fsqr_ctx* ctx, int32_t r, int32_t t, int64_t cap, int
     CK(cudaMemcpy(beta_host, ctx->D.path_beta + q * ctx->path_cap, sizeof(double) * m, cudaMemcpyDeviceToHost));
     for (int64_t a = 0; a < m; ++a) idx_host[a] = ii[a];
   }
+  if (cnt > ctx->path_cap)
+    return set_err(ctx, FSQR_ERR_STATE,
+                   "path point (rhs %d, t %d) has %lld nonzero coefficients, more than the path store holds "
+                   "(%lld = min(p+1, 4n+64)); the first %lld in index order were returned",
+                   r, t, cnt, (long long)ctx->path_cap, (long long)m);
   return FSQR_OK;
 }
 
 fsqr_status fsqr_trace(fsqr_ctx* ctx, double* out_host, int64_t cap_rows, int64_t* rows) {
   if (!ctx || !out_host || !rows) return set_err(ctx, FSQR_ERR_CONFIG, "null argument");
+  SYNC_DEVICE();
   long long it = 0;
   int stopped = 0;
   CK(cudaMemcpy(&it, ctx->D.iter, sizeof it, cudaMemcpyDeviceToHost));
@@ -1248,6 +1250,7 @@ fsqr_status fsqr_profile_iterate(fsqr_ctx* ctx, int64_t k, double* stage_ms_host
 
 int64_t fsqr_iterations(fsqr_ctx* ctx) {
   if (!ctx) return -1;
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
   long long it = 0;
   if (cudaMemcpy(&it, ctx->D.iter, sizeof it, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
   return it;

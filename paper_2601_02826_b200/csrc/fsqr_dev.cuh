@@ -26,14 +26,17 @@
 #define FIN_MAXGRID 256       // ceil(65536 / FIN_THREADS)
 #define FSQR_PATH_W 8         // path record: iters, Rp, Rb, Rz, obj, nnz, converged, loss sum
 
-enum { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_NUMERIC = 3 };
+// ST_SWITCH: path mode, w^k was just recorded as point t and becomes the start of point t+1
+// (reading R10): the update of iteration k (taken with lambda_t) is discarded -- K1 and finalize
+// skip the RHS, K2's last CTA restored beta^k into the next parity -- and finalize's tail sets the
+// RHS active again, so iteration k+1 re-tests w^k at lambda_{t+1}.
+enum { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_NUMERIC = 3, ST_SWITCH = 4 };
 
 struct Dev {
   // sizes / layout
   int n, R, G, storage, npad, ldk;
   int k1_esmax;                     // k1_tcp: support entries per work item cap (<= 65536; FSQR_K1_ESMAX, tests)
-  int k1_tc;                        // forward product: 0 k1_bulk (CUDA cores), 1 k1_tc (TMEM transpose), 2 k1_tcg (gather4), 3 k1_tcp (2-bit, smem unpack)
-  const void* tmG;                  // host pointer to the gather4 tensor map (launcher side only)
+  int k1_tc;                        // forward product: 0 k1_bulk (CUDA cores), 3 k1_tcp 2-bit, 4 k1_tcp u8 (tensor cores)
   int x_policy;                     // L2 hint of the X stream in K2: 0 evict_first, 1 normal, 2 evict_last
   int k1_policy;                    // L2 hint of the forward gather: 0 evict_first, 1 normal, 2 evict_last
   int bperm;                        // 1: theta digit rows in the 2-bit tcgen05 K order (k2_tc2.cu)
@@ -500,10 +503,6 @@ void launch_unpack2(const uint8_t* x2, int64_t ld2, int64_t p, uint8_t* x8, int6
 int k2_tc_smem_bytes(int npad);
 cudaError_t k2_tc_init();
 cudaError_t k1_init();
-cudaError_t k1_tc_init();
-cudaError_t k1_tcg_init();
-void launch_k1_tcg(const Dev& D, const void* tmG, int grid, cudaStream_t st, int cur);
-void launch_k1_tc(const Dev& D, int grid, cudaStream_t st, int cur);
 void launch_k1_tcp(const Dev& D, int grid, cudaStream_t st, int cur);
 cudaError_t k1_tcp_init();
 int k2_tc_supported(int npad);

@@ -424,16 +424,8 @@ cudaError_t init_r() {
 
 // grid = number of SMs; the bulk kernel scales it by its resident CTAs per SM
 void launch_k1_mode(const Dev& D, int grid, cudaStream_t st, int cur) {
-  if (D.k1_tc == 2 && D.storage == 1) {
-    launch_k1_tcg(D, D.tmG, grid, st, cur);
-    return;
-  }
   if ((D.k1_tc == 3 && D.storage == 2) || (D.k1_tc == 4 && D.storage == 1)) {
     launch_k1_tcp(D, grid, st, cur);
-    return;
-  }
-  if (D.k1_tc == 1 && D.storage != 0) {
-    launch_k1_tc(D, grid, st, cur);
     return;
   }
   if (D.R <= 1) launch_r<1>(D, grid, st, cur);

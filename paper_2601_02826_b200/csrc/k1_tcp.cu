@@ -2,7 +2,8 @@
 // the support of beta^{k+1} ("computation of X beta ... divided into G
 // simultaneous sub-tasks ... followed by computing their sum"), exact integer arithmetic.
 //
-//   S_{i,r} = sum_{j in S} x_ij C_{j,r} = sum_k 256^k D_{i,(r,k)},   D = X_S · Dig   (see k1_tc.cu)
+//   S_{i,r} = sum_{j in S} x_ij C_{j,r} = sum_k 256^k D_{i,(r,k)},   D = X_S · Dig,
+// C_{j,r} = round(2^E beta_{j,r} / s_j) in six balanced base-256 digits (k1_fwd.cu)
 //
 // GEMM D[M = rows][N = digit columns] = A[rows][K = support] · B, A MN-major (X is SNP-major:
 // each column's rows are contiguous).  The CUDA-core kernel k1_bulk spends ~4 instructions per

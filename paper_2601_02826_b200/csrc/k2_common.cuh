@@ -144,6 +144,8 @@ __device__ void k2_finish(const Dev& D, const K2Ctx<RMAX>& C, K2Part<RMAX>& P, d
               D.status[r] = conv ? ST_CONVERGED : ST_MAXITER;
               D.commit_iter[r] = C.k;
             } else {
+              // w^k initialises lambda_{t+1} (L412): discard this iteration's update for r
+              D.status[r] = ST_SWITCH;
               D.t_idx[r] = t + 1;
               D.lam_cur[r] = D.lam_path[(size_t)r * D.T + t + 1];
               D.pt_iters[r] = 0;
@@ -164,46 +166,70 @@ __device__ void k2_finish(const Dev& D, const K2Ctx<RMAX>& C, K2Part<RMAX>& P, d
     }
   }
   __syncthreads();
-  // ---------------- path: copy the sparse solution beta^k (support list of parity k) of recorded RHS
+  // ---------------- path: the sparse solution beta^k of each recorded RHS, in index order
+  // (deterministic: a block-wide ordered compaction of the dense column), capped at path_cap
+  // (the true count is stored; fsqr_path_beta reports truncation).  An RHS that switches lambda
+  // also gets beta^k copied over the beta^{k+1} this pass wrote (ST_SWITCH).
   if (D.update && D.path) {
-    const int par = (int)(C.k & 1);
-    const int cnt = D.sup_cnt[par];
-    __shared__ int s_cnt;
+    constexpr int E = 4;   // consecutive coefficients per thread and step
+    __shared__ int s_wtot[32];
+    __shared__ long long s_base;
     for (int r = 0; r < C.R; ++r) {
       const int t = s_rec[r];
       if (t < 0) continue;
-      if (tid == 0) s_cnt = 1;
-      __syncthreads();
+      const bool sw = D.status[r] == ST_SWITCH;
       const size_t base = ((size_t)r * D.T + t) * D.path_cap;
-      if (tid == 0) {
-        D.path_idx[base] = 0;
-        D.path_beta[base] = C.beta_in[r];
-      }
-      for (int e0 = 0; e0 < cnt; e0 += blockDim.x) {
-        const int e = e0 + tid;
-        double bv = 0.0;
-        int jj = 0;
-        if (e < cnt) {
-          bv = D.sup_b[par][(size_t)e * D.R + r];
-          jj = D.sup_idx[par][e] + 1;
+      if (tid == 0) s_base = 0;
+      __syncthreads();
+      for (int64_t j0 = 0; j0 <= D.p; j0 += (int64_t)E * blockDim.x) {
+        double v[E];
+        int c = 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int64_t j = j0 + (int64_t)E * tid + e;
+          v[e] = 0.0;
+          if (j <= D.p) {
+            v[e] = C.beta_in[j * C.R + r];
+            if (sw) C.beta_out[j * C.R + r] = v[e];
+          }
+          c += v[e] != 0.0;
         }
-        if (bv != 0.0) {
-          const int slot = atomicAdd(&s_cnt, 1);
-          if (slot < D.path_cap) {
-            D.path_idx[base + slot] = jj;
-            D.path_beta[base + slot] = bv;
+        int incl = c;   // inclusive warp scan of the per-thread counts
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += u;
+        }
+        if (lane == 31) s_wtot[wid] = incl;
+        __syncthreads();
+        long long off = s_base + incl - c;
+        for (int w = 0; w < wid; ++w) off += s_wtot[w];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if (v[e] != 0.0) {
+            if (off < D.path_cap) {
+              D.path_idx[base + off] = (int32_t)(j0 + (int64_t)E * tid + e);
+              D.path_beta[base + off] = v[e];
+            }
+            ++off;
           }
         }
+        __syncthreads();
+        if (tid == 0) {
+          long long tot = 0;
+          for (int w = 0; w < nw; ++w) tot += s_wtot[w];
+          s_base += tot;
+        }
+        __syncthreads();
       }
-      __syncthreads();
-      if (tid == 0) D.path_cnt[(size_t)r * D.T + t] = s_cnt;
+      if (tid == 0) D.path_cnt[(size_t)r * D.T + t] = s_base;
       __syncthreads();
     }
   }
   if (tid == 0) {
     if (D.update) {
       int any = 0;
-      for (int r = 0; r < D.R; ++r) any |= (D.status[r] == ST_ACTIVE);
+      for (int r = 0; r < D.R; ++r) any |= (D.status[r] == ST_ACTIVE || D.status[r] == ST_SWITCH);
       *D.stop = any ? 0 : 1;
     }
     *D.ticket = 0u;

@@ -198,7 +198,10 @@ __global__ void __launch_bounds__(FT) k_finalize(const Dev D) {
     nvec_step(D, r, 0, b0, par1, smd, smll);
   }
   __syncthreads();
-  if (threadIdx.x < D.R) D.cmax[par * D.R + threadIdx.x] = 0ull;
+  if (threadIdx.x < D.R) {
+    D.cmax[par * D.R + threadIdx.x] = 0ull;
+    if (D.status[threadIdx.x] == ST_SWITCH) D.status[threadIdx.x] = ST_ACTIVE;   // re-test w^k at lambda_{t+1}
+  }
   if (threadIdx.x == 0) {
     D.sup_cnt[par] = 0;
     *D.iter = k + 1;
@@ -362,7 +365,10 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize_mc(const Dev D) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  if (threadIdx.x < D.R) D.cmax[par * D.R + threadIdx.x] = 0ull;
+  if (threadIdx.x < D.R) {
+    D.cmax[par * D.R + threadIdx.x] = 0ull;
+    if (D.status[threadIdx.x] == ST_SWITCH) D.status[threadIdx.x] = ST_ACTIVE;   // re-test w^k at lambda_{t+1}
+  }
   if (threadIdx.x == 0) {
     D.sup_cnt[par] = 0;
     *D.iter = k + 1;

@@ -44,3 +44,97 @@ def rel(a, b):
 def support_mismatch(beta_gpu, beta_orc, g_margin=None):
     """Indices where exactly one side is zero."""
     return np.flatnonzero((beta_gpu != 0) != (beta_orc != 0))
+
+
+# ------------------------------------------------------------------ numpy one-step checker (test-local)
+# Written from the paper's formulas (E14, E15, E12); it never calls the oracle, whose inputs never
+# come from the CUDA path, so it can check a GPU step taken from any GPU state.
+
+def raw_columns(prob, cols):
+    """fp64 codes [len(cols), n] of the stored data columns (any storage)."""
+    Xc = prob.X[cols]
+    if prob.storage == datagen.STORAGE_P2:
+        codes = (Xc[:, :, None] >> (2 * np.arange(4, dtype=np.uint8))) & 3
+        return codes.reshape(len(cols), -1)[:, : prob.n].astype(np.float64)
+    return Xc[:, : prob.n].astype(np.float64)
+
+
+def block_of(j, p1, G):
+    """DESIGN.md R6: contiguous blocks, the first (p+1) mod G one column larger."""
+    q, rem = p1 // G, p1 % G
+    big = rem * (q + 1)
+    j = np.asarray(j)
+    return np.where(j < big, j // (q + 1), rem + (j - big) // max(q, 1))
+
+
+def prox_beta_np(b, g, lam, eta):
+    a = eta * b + g
+    return (np.maximum(a - lam, 0.0) - np.maximum(-a - lam, 0.0)) / eta
+
+
+def forward_np(prob, beta_col):
+    """s = X~ beta over the nonzero model columns (beta_col: [p+1])."""
+    s = np.full(prob.n, beta_col[0])
+    nz = np.flatnonzero(beta_col[1:] != 0.0)
+    for a in range(0, len(nz), 2048):
+        cols = nz[a:a + 2048]
+        raw = raw_columns(prob, cols)
+        m = raw.mean(axis=1)
+        sd = raw.std(axis=1, ddof=1)
+        s += ((raw - m[:, None]) / sd[:, None]).T @ beta_col[cols + 1]
+    return s
+
+
+def check_one_step(prob, S, taus, lams, eta, mu, G, seed=7, ncols=4000):
+    import paper_2601_02826_b200 as fs
+
+    b0, z0, t0 = S.state()
+    fs.fsqr_profile_iterate(S.ctx, 1)          # exactly the launches bench.py times
+    b1, z1, t1 = S.state()
+    R, n, p = len(taus), prob.n, prob.p
+    rng = np.random.default_rng(seed)
+    sup = np.flatnonzero((b0[:, 1:] != 0).any(axis=0) | (b1[:, 1:] != 0).any(axis=0))
+    cols = np.union1d(rng.choice(p, size=min(ncols, p), replace=False), sup)
+    n_checked = 0
+    for a in range(0, len(cols), 2048):
+        cc = cols[a:a + 2048]
+        raw = raw_columns(prob, cc)
+        m = raw.mean(axis=1)
+        sd = raw.std(axis=1, ddof=1)
+        xt = (raw - m[:, None]) / sd[:, None]
+        g = xt @ t0.T                      # [c, R]
+        gabs = np.abs(xt) @ np.abs(t0).T   # dot-product error scale
+        j = cc + 1
+        e = eta[block_of(j, p + 1, G)]
+        for r in range(R):
+            exp = prox_beta_np(b0[r, j], g[:, r], lams[r], e)
+            err = np.abs(b1[r, j] - exp)
+            bound = 1e-5 * gabs[:, r] / e + 1e-300
+            assert np.all(err <= bound), (r, int(np.argmax(err / bound)), float(np.max(err / bound)))
+            margin = np.abs(np.abs(e * b0[r, j] + g[:, r]) - lams[r])
+            clear = margin > 1e-6 * lams[r]
+            assert np.array_equal((b1[r, j] != 0)[clear], (exp != 0)[clear])
+            n_checked += len(j)
+    # intercept (lambda_0 = 0, block 1)
+    for r in range(R):
+        exp0 = b0[r, 0] + t0[r].sum() / eta[0]
+        assert abs(b1[r, 0] - exp0) <= 1e-5 * np.abs(t0[r]).sum() / eta[0]
+    # rows: E15 for z, E12 for theta with s = X~ beta recomputed from the bytes
+    sigma = mu / (G + 1)
+    for r in range(R):
+        tau = taus[r]
+        v = z0[r] + t0[r] / mu
+        z_exp = np.maximum(v - tau / (n * mu), 0.0) - np.maximum(-v - (1 - tau) / (n * mu), 0.0)
+        np.testing.assert_allclose(z1[r], z_exp, rtol=1e-12, atol=1e-12 * np.abs(z_exp).max())
+        s0 = forward_np(prob, b0[r])
+        s1 = forward_np(prob, b1[r])
+        r0 = s0 + z0[r] - prob.y
+        r1 = s1 + z1[r] - prob.y
+        dth = -sigma * (2 * r1 - r0)
+        # E12 consumes the forward products s^k, s^{k+1}: with those within north_star's product
+        # tolerance (1e-5 relative) the dual step can differ by at most sigma (2 |ds1| + |ds0|)
+        err = np.linalg.norm((t1[r] - t0[r]) - dth)
+        assert err <= 1e-5 * sigma * (2 * np.linalg.norm(s1) + np.linalg.norm(s0)), (err, np.linalg.norm(dth))
+    return n_checked, len(sup)
+
+

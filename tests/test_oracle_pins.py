@@ -227,6 +227,63 @@ def test_kkt_certificate_and_fixed_point():
         assert np.max(np.abs(a - b)) < 1e-8
 
 
+def _kkt_example():
+    c = GOLD["kkt_example"]
+    X = np.zeros((1, 16), np.uint8)
+    X[0, :3] = [0, 1, 2]
+    d = oracle.Design(1, 3, 1, 16, X)
+    return c, d
+
+
+def test_kkt_rel_hand_example():
+    """R = (R_p, R_beta, R_z) of reading R1 on a 3-observation example derived by hand
+    (tests/golden/worked_values.json "kkt_example"): pins every normalisation term."""
+    c, d = _kkt_example()
+    np.testing.assert_allclose(d.mean, [1.0])
+    np.testing.assert_allclose(d.sd, [1.0])
+    R = oracle.kkt_rel(d, c["y"], c["tau"], c["lam"], c["beta"], c["z"], c["theta"])
+    np.testing.assert_allclose(R, c["expect_R"], rtol=1e-14)
+
+
+def test_kkt_cert_hand_example_negative():
+    """The Prop. 1 certificate is not trivially zero: at the (non-optimal) hand example it returns
+    the violations derived by hand."""
+    c, d = _kkt_example()
+    cert = oracle.kkt_cert(d, c["y"], c["tau"], c["lam"], c["beta"], c["z"], c["theta"])
+    np.testing.assert_allclose(cert, c["expect_cert"], rtol=1e-14)
+
+
+@pytest.mark.parametrize("seed,tau,lfrac", [(31, 0.5, 0.2), (32, 0.25, 0.1), (33, 0.8, 0.4)])
+def test_kkt_zero_at_lp_saddle_point(seed, tau, lfrac):
+    """At the LP optimum with theta* from the LP's equality duals (an exact saddle point of
+    Prop. 1), R(w*) vanishes and the certificate is zero; moving one inactive coefficient off zero
+    by delta gives exactly the violations that move predicts."""
+    prob, d = _tiny(seed, n=30, p=40, tau=tau)
+    A, _, _ = _np_standardized(prob)
+    lm, _ = oracle.lambda_max(d, prob.y, tau)
+    lam = oracle.lam_vector(prob.p, lfrac * lm)
+    beta, z, theta = lp.highs_saddle(A, prob.y, tau, lam)
+    assert np.all(theta >= (tau - 1) / prob.n - 1e-12) and np.all(theta <= tau / prob.n + 1e-12)
+    R = oracle.kkt_rel(d, prob.y, tau, lam, beta, z, theta)
+    assert R.max() <= 1e-9, R
+    cert = oracle.kkt_cert(d, prob.y, tau, lam, beta, z, theta)
+    assert cert.max() <= 1e-9, cert
+    g = A.T @ theta
+    inactive = [j for j in range(1, prob.p + 1) if beta[j] == 0.0 and abs(g[j]) < lam[j] - 1e-9]
+    assert inactive
+    j, delta = inactive[0], 1e-3
+    b2 = beta.copy()
+    b2[j] = delta
+    cert2 = oracle.kkt_cert(d, prob.y, tau, lam, b2, z, theta)
+    assert cert2[0] == pytest.approx(delta * np.abs(A[:, j]).max(), rel=1e-6)   # z = y - X~beta broken
+    assert cert2[1] == pytest.approx(max(cert[1], abs(g[j] - lam[j])), rel=1e-6)   # g_j != lam_j sign(beta_j)
+    R2 = oracle.kkt_rel(d, prob.y, tau, lam, b2, z, theta)
+    # R_p: ||X~_j delta|| / (1 + ||y||); R_beta: the moved coordinate is pulled back to S_lam(delta + g_j) = 0
+    assert R2[0] == pytest.approx(delta * np.linalg.norm(A[:, j]) / (1 + np.linalg.norm(prob.y)), rel=1e-5)
+    bb, gg = np.linalg.norm(b2), np.linalg.norm(g)
+    assert R2[1] == pytest.approx(delta / (1 + bb + gg), rel=1e-5)
+
+
 def test_lambda_max_null_model():
     """At lambda >= lambda_max the solution is beta_{1..p} = 0 with intercept = the sample
     tau-quantile (textbook); just below it, some beta_j != 0."""
@@ -336,6 +393,32 @@ def test_path_warm_start_semantics():
                             max_iter=300000, tol=1e-9)
         assert cold["status"] == 0
         assert res["obj"][t] == pytest.approx(cold["obj"], rel=1e-6)
+
+
+def test_path_is_chained_warm_solves():
+    """Reading R10 (L412, "the solution from the preceding lambda serves as the initialization"):
+    point t+1 of the path starts from the iterate recorded as point t, so the path equals a chain
+    of Algorithm-1 solves, each started from the previous one's output -- same update counts and
+    bitwise-identical solutions, including points capped by max_iter_point."""
+    prob = datagen.make("c2", n=50, p=70, seed=73)
+    d = oracle.Design.from_problem(prob)
+    tau, G, mu = 0.3, 4, 0.04
+    eta = oracle.eta(d, G, mu)
+    lm, _ = oracle.lambda_max(d, prob.y, tau)
+    lam_path = lm * 1.01 * (0.05 ** (np.arange(5) / 4))
+    cap = 400
+    res = oracle.path(d, prob.y, tau, lam_path, eta, mu, G, tol=1e-6, max_iter_point=cap)
+    state = None
+    for t in range(5):
+        o = oracle.solve(d, prob.y, tau, oracle.lam_vector(prob.p, lam_path[t]), eta, mu, G, max_iter=cap,
+                         tol=1e-6, state=state)
+        assert res["iters"][t] == o["iters"], t
+        assert res["converged"][t] == (o["status"] == 0)
+        np.testing.assert_array_equal(res["beta_path"][t], o["beta"])
+        state = (o["beta"], o["z"], o["theta"])
+    assert res["total"] == res["iters"].sum()
+    assert not res["converged"].all()     # the cap closed at least one point
+    np.testing.assert_array_equal(res["beta"], state[0])
 
 
 # ----------------------------------------------------------------- Section 5 (LLA) and HBIC pins
