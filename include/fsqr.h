@@ -209,6 +209,14 @@ fsqr_status fsqr_set_state(fsqr_ctx* ctx, const double* beta_host, const double*
 /* change the penalty level per RHS (lambda_host [n_rhs]); the state is kept (warm start). */
 fsqr_status fsqr_set_lambda(fsqr_ctx* ctx, const double* lambda_host);
 
+/* change the stopping tolerance (tol > 0) and the per-call iteration cap (max_iter >= 0) of
+ * fsqr_solve / fsqr_lla / fsqr_path's stopping test; the state is kept.  Waits for the device. */
+fsqr_status fsqr_set_tolerance(fsqr_ctx* ctx, double tol, int64_t max_iter);
+
+/* kernel launches per outer iteration on the hot path (2: X~^T theta pass + forward product with
+ * the fused finalize; 3 when the finalize runs as its own kernel, e.g. fp32 storage). */
+int32_t fsqr_launches_per_iteration(const fsqr_ctx* ctx);
+
 /* lambda_max(tau) per RHS (null-model threshold, reading R4), computed on the GPU at create. */
 fsqr_status fsqr_lambda_max(const fsqr_ctx* ctx, double* out_host);
 
@@ -234,6 +242,34 @@ fsqr_status fsqr_path(fsqr_ctx* ctx, const double* lam_path_host, int32_t T, int
  * |A| (log log n / n) log p at the recorded iterate (the paper's lambda selection in sparse
  * settings, L406-411).  FSQR_ERR_STATE before fsqr_path. */
 fsqr_status fsqr_path_hbic(fsqr_ctx* ctx, double* hbic_host);
+
+/*
+ * The paper's tuning protocol for sparse settings, one call: per RHS r
+ *   1. the grid top: lambda_max(tau_r) (reading R4); with B > 0 also the pivotal lambda
+ *      lambda_piv = c * q_{1-alpha}(Lambda_1..Lambda_B) of fsqr_pivotal (reading R18; the order
+ *      statistic ceil((1-alpha) B) of the sorted Lambda_b; c = 1.1, alpha = 0.1 in B-C);
+ *   2. a geometric grid of T points from lam_hi = max(lambda_max, lambda_piv) down to
+ *      lam_lo = lam_min_frac * min(lambda_max, lambda_piv) (reading R20; B = 0: lambda_max to
+ *      lam_min_frac * lambda_max), written to grid_host [n_rhs][T];
+ *   3. the warm-started path over that grid (fsqr_path, "the solution from the preceding lambda
+ *      serves as the initialization", L412) from the context's current state;
+ *   4. HBIC (E18, L408-411) of every point into hbic_host [n_rhs][T] and its argmin (the first
+ *      minimal point) into best_host [n_rhs]; the selected solution is fsqr_path_beta(r, best).
+ * lam_piv_host [n_rhs] receives lambda_piv (0 when B = 0); total the lockstep passes over X.
+ * Any output pointer may be NULL except best_host.  Blocking.  Errors: FSQR_ERR_CONFIG for
+ * T < 2, lam_min_frac not in (0, 1), B < 0, alpha not in (0, 1) or c <= 0.
+ */
+typedef struct {
+  int32_t T;             /* grid points per RHS (the paper: 50) */
+  int32_t pad_;
+  double lam_min_frac;   /* bottom of the grid (see 2.) */
+  int64_t B;             /* pivotal replicates (0: no pivotal statistic) */
+  uint64_t seed;         /* pivotal draws */
+  double alpha, c;       /* lambda_piv = c * q_{1-alpha}(Lambda) */
+} fsqr_tune_options;
+
+fsqr_status fsqr_tune(fsqr_ctx* ctx, const fsqr_tune_options* o, double* grid_host, double* hbic_host,
+                      int32_t* best_host, double* lam_piv_host, int64_t* total, void* stream);
 
 /* Sparse solution of path point t for RHS r: writes up to cap (index j, beta_j standardised) pairs
  * in ascending j (deterministic), returns the count of nonzeros in *count (which may exceed cap:

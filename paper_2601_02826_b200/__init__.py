@@ -50,6 +50,11 @@ class fsqr_options(ctypes.Structure):
                 ("power_tol", ctypes.c_double), ("seed", ctypes.c_uint64), ("max_iter_point", ctypes.c_int64)]
 
 
+class fsqr_tune_options(ctypes.Structure):
+    _fields_ = [("T", ctypes.c_int32), ("pad_", ctypes.c_int32), ("lam_min_frac", ctypes.c_double),
+                ("B", ctypes.c_int64), ("seed", ctypes.c_uint64), ("alpha", ctypes.c_double), ("c", ctypes.c_double)]
+
+
 class fsqr_result(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int64), ("total_iterations", ctypes.c_int64), ("n_rhs", ctypes.c_int32),
                 ("status", ctypes.c_int32 * 16), ("R", (ctypes.c_double * 3) * 16),
@@ -60,7 +65,7 @@ EXPORTS = ["fsqr_default_options", "fsqr_create", "fsqr_iterate", "fsqr_solve", 
            "fsqr_get_beta", "fsqr_get_state", "fsqr_set_state", "fsqr_set_lambda", "fsqr_lambda_max",
            "fsqr_get_eta", "fsqr_get_colstats", "fsqr_path", "fsqr_path_beta", "fsqr_trace", "fsqr_iterations",
            "fsqr_profile_iterate", "fsqr_hbic", "fsqr_set_lambda_weights", "fsqr_lla", "fsqr_pivotal", "fsqr_set_lambda2", "fsqr_path_hbic",
-           "fsqr_backend_name", "fsqr_fit_host", "fsqr_pack2", "fsqr_last_error", "fsqr_global_error", "fsqr_status_str",
+           "fsqr_tune", "fsqr_set_tolerance", "fsqr_launches_per_iteration", "fsqr_backend_name", "fsqr_fit_host", "fsqr_pack2", "fsqr_last_error", "fsqr_global_error", "fsqr_status_str",
            "fsqr_destroy"]
 
 
@@ -107,9 +112,13 @@ def load(build_if_missing: bool = True):
     L.fsqr_hbic.argtypes = [ctxp, P, P]
     L.fsqr_set_lambda2.argtypes = [ctxp, P]
     L.fsqr_path_hbic.argtypes = [ctxp, P]
+    L.fsqr_tune.argtypes = [ctxp, ctypes.POINTER(fsqr_tune_options), P, P, P, P, P, P]
     L.fsqr_pivotal.argtypes = [ctxp, I32, I64, ctypes.c_uint64, P, P]
     L.fsqr_set_lambda_weights.argtypes = [ctxp, P, P]
     L.fsqr_lla.argtypes = [ctxp, I32, D, I32, P, ctypes.POINTER(fsqr_result), P]
+    L.fsqr_set_tolerance.argtypes = [ctxp, D, I64]
+    L.fsqr_launches_per_iteration.argtypes = [ctxp]
+    L.fsqr_launches_per_iteration.restype = I32
     L.fsqr_iterations.argtypes = [ctxp]
     L.fsqr_iterations.restype = I64
     L.fsqr_backend_name.argtypes = [ctxp]
@@ -128,7 +137,8 @@ def load(build_if_missing: bool = True):
     for name in ("fsqr_create", "fsqr_iterate", "fsqr_solve", "fsqr_objective", "fsqr_kkt", "fsqr_get_beta",
                  "fsqr_get_state", "fsqr_set_state", "fsqr_set_lambda", "fsqr_lambda_max", "fsqr_get_eta",
                  "fsqr_get_colstats", "fsqr_path", "fsqr_path_beta", "fsqr_trace", "fsqr_fit_host", "fsqr_hbic",
-                 "fsqr_set_lambda_weights", "fsqr_lla", "fsqr_pivotal", "fsqr_set_lambda2", "fsqr_path_hbic", "fsqr_pack2"):
+                 "fsqr_set_lambda_weights", "fsqr_lla", "fsqr_pivotal", "fsqr_set_lambda2", "fsqr_path_hbic", "fsqr_pack2",
+                 "fsqr_tune", "fsqr_set_tolerance"):
         getattr(L, name).restype = S
     _lib = L
     return L
@@ -276,6 +286,20 @@ def fsqr_path_hbic(ctx, n_rhs: int, T: int) -> np.ndarray:
     return out
 
 
+def fsqr_tune(ctx, n_rhs: int, T: int = 50, lam_min_frac: float = 0.01, B: int = 0, seed: int = 0x5EED,
+              alpha: float = 0.1, c: float = 1.1, stream=None) -> dict:
+    """The tuning protocol (L406-412) in one C-ABI call: grid, warm-started path, HBIC, argmin."""
+    o = fsqr_tune_options(int(T), 0, float(lam_min_frac), int(B), int(seed) & 0xFFFFFFFFFFFFFFFF, float(alpha),
+                          float(c))
+    grid, h = np.zeros((n_rhs, T)), np.zeros((n_rhs, T))
+    best = np.zeros(n_rhs, dtype=np.int32)
+    piv = np.zeros(n_rhs)
+    total = ctypes.c_int64(0)
+    _check(load().fsqr_tune(ctx, ctypes.byref(o), _ptr(grid), _ptr(h), _ptr(best), _ptr(piv), ctypes.byref(total),
+                            _stream(stream)), ctx)
+    return dict(grid=grid, hbic=h, best=best.astype(np.int64), lam_piv=piv, total=total.value)
+
+
 def fsqr_path_beta(ctx, r: int, t: int, p: int) -> np.ndarray:
     """Dense standardised beta (length p+1) of path point t of RHS r."""
     cap = p + 1
@@ -335,6 +359,14 @@ def fsqr_pivotal(ctx, rhs: int, B: int, seed: int = 0x5EED, stream=None) -> np.n
     out = np.empty(int(B))
     _check(load().fsqr_pivotal(ctx, int(rhs), int(B), ctypes.c_uint64(int(seed)), _ptr(out), _stream(stream)), ctx)
     return out
+
+
+def fsqr_set_tolerance(ctx, tol: float, max_iter: int):
+    return _check(load().fsqr_set_tolerance(ctx, float(tol), int(max_iter)), ctx)
+
+
+def fsqr_launches_per_iteration(ctx) -> int:
+    return int(load().fsqr_launches_per_iteration(ctx))
 
 
 def fsqr_iterations(ctx) -> int:
@@ -397,6 +429,7 @@ class Solver:
         self.y = y if isinstance(y, torch.Tensor) else torch.as_tensor(np.asarray(y, np.float64), device="cuda")
         self.lambda_w = lambda_w
         self.n, self.p, self.R, self.G = int(n), int(p), len(taus), int(G)
+        self.max_iter = int(max_iter)
         self.taus = list(taus)
         opt = default_options(G=G, mu=mu, tol=tol, max_iter=max_iter, backend=backend,
                               max_iter_point=max_iter_point, **kw)
@@ -448,24 +481,13 @@ class Solver:
     def path_hbic(self, T: int):
         return fsqr_path_hbic(self.ctx, self.R, T)
 
-    def tune(self, T: int = 50, lam_min_frac: float = 0.01, B: int = 0, seed: int = 0x5EED):
-        """The paper's tuning protocol for sparse settings (L406-412) on the GPU: a warm-started
-        geometric lambda path of T points per tau, from lambda_max (or, with B > 0 replicates, from
-        the pivotal lambda of reading R18 up to lambda_max) down to lam_min_frac times its top,
-        HBIC (E18) of every point, and the minimiser.  Returns dict(grid, hbic, best, beta)."""
-        lm = np.asarray(self.lambda_max())
-        top = lm.copy()
-        if B > 0:
-            for r in range(self.R):
-                L = fsqr_pivotal(self.ctx, r, B, seed)
-                s = np.sort(L)
-                top[r] = max(lm[r], 1.1 * s[int(np.ceil(0.9 * B)) - 1])
-        grid = np.array([[top[r] * lam_min_frac ** (t / (T - 1)) for t in range(T)] for r in range(self.R)])
-        res = self.path(grid)
-        h = self.path_hbic(T)
-        best = np.argmin(h, axis=1)
-        beta = np.stack([self.path_beta(r, int(best[r])) for r in range(self.R)])
-        return dict(grid=grid, path=res, hbic=h, best=best, beta=beta)
+    def tune(self, T: int = 50, lam_min_frac: float = 0.01, B: int = 0, seed: int = 0x5EED, alpha: float = 0.1,
+             c: float = 1.1):
+        """fsqr_tune: returns dict(grid, hbic, best, lam_piv, total, beta) where beta
+        [n_rhs, p+1] is the HBIC-selected point of each RHS (fsqr_path_beta)."""
+        out = fsqr_tune(self.ctx, self.R, T, lam_min_frac, B, seed, alpha, c)
+        out["beta"] = np.stack([self.path_beta(r, int(out["best"][r])) for r in range(self.R)])
+        return out
 
     def path_beta(self, r: int, t: int):
         return fsqr_path_beta(self.ctx, r, t, self.p)
@@ -487,6 +509,13 @@ class Solver:
 
     def trace(self, rows: int = 4096):
         return fsqr_trace(self.ctx, self.R, rows)
+
+    def set_tol(self, tol: float, max_iter: int | None = None):
+        self.max_iter = self.max_iter if max_iter is None else int(max_iter)
+        return fsqr_set_tolerance(self.ctx, tol, self.max_iter)
+
+    def launches_per_iteration(self) -> int:
+        return fsqr_launches_per_iteration(self.ctx)
 
     def iterations(self) -> int:
         return fsqr_iterations(self.ctx)

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfsqr.so")
 SOURCES = ["fsqr_api.cu", "k2_tc.cu", "k2_tc2.cu", "k2_simt.cu", "k1_fwd.cu", "k1_tcp.cu", "kfin.cu", "k_pivotal.cu"]
-HEADERS = ["fsqr_dev.cuh", "k2_common.cuh"]
+HEADERS = ["fsqr_dev.cuh", "k2_common.cuh", "fin_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
 

@@ -193,7 +193,7 @@ void launch_k2(fsqr_ctx* ctx, const Dev& D, cudaStream_t st) {
 void enqueue_iteration(fsqr_ctx* ctx, const Dev& D, cudaStream_t st) {
   launch_k2(ctx, D, st);
   launch_k1(D, ctx->k1_grid, st);
-  launch_finalize(D, st);
+  if (!k1_fuses_finalize(D)) launch_finalize(D, st);
 }
 
 fsqr_status get_graph(fsqr_ctx* ctx, int mode, Graph** out) {
@@ -239,6 +239,8 @@ fsqr_status init_state(fsqr_ctx* ctx, cudaStream_t st) {
   CK(cudaMemsetAsync(D.cmax, 0, 2 * ctx->R * sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(D.sacc, 0, (size_t)ctx->R * ctx->n * sizeof(long long), st));
   CK(cudaMemsetAsync(D.mterm, 0, ctx->R * sizeof(long long), st));
+  CK(cudaMemsetAsync(D.k1bar, 0, sizeof(unsigned), st));
+  CK(cudaMemsetAsync(D.fticket, 0, (1 + FSQR_MAXR) * sizeof(unsigned), st));
   CK(cudaMemsetAsync(D.stop, 0, sizeof(int), st));
   if (D.storage != 0) launch_build_support(D, par, st);
   launch_k1_mode(D, ctx->k1_grid, st, 1);
@@ -586,6 +588,7 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
   AL(D.cmax, 2 * R);
   AL(D.sacc, nR);
   AL(D.mterm, R);
+  AL(D.k1bar, 1);
   AL(D.k2part, (size_t)std::max(ctx->k2_grid, ctx->sms * 8) * R * FSQR_NPART);
   AL(D.ticket, 1);
   AL(D.kbase, 1);
@@ -1060,6 +1063,31 @@ fsqr_status fsqr_set_lambda(fsqr_ctx* ctx, const double* lambda_host) {
   return FSQR_OK;
 }
 
+fsqr_status fsqr_set_tolerance(fsqr_ctx* ctx, double tol, int64_t max_iter) {
+  if (!ctx) return set_err(nullptr, FSQR_ERR_CONFIG, "ctx is NULL");
+  if (!(tol > 0.0) || !std::isfinite(tol) || max_iter < 0)
+    return set_err(ctx, FSQR_ERR_CONFIG, "need tol > 0 and max_iter >= 0");
+  SYNC_DEVICE();
+  ctx->opt.tol = tol;
+  ctx->opt.max_iter = max_iter;
+  ctx->D.tol = tol;
+  ctx->D.max_iter = max_iter;
+  for (int m = 0; m < M_COUNT; ++m) {   // the captured graphs bake the kernel parameters
+    ctx->mode_dev[m].tol = tol;
+    ctx->mode_dev[m].max_iter = max_iter;
+    if (ctx->graph[m].exec) {
+      cudaGraphExecDestroy(ctx->graph[m].exec);
+      ctx->graph[m].exec = nullptr;
+    }
+  }
+  return FSQR_OK;
+}
+
+int32_t fsqr_launches_per_iteration(const fsqr_ctx* ctx) {
+  if (!ctx) return -1;
+  return k1_fuses_finalize(ctx->mode_dev[M_ITER]) ? 2 : 3;
+}
+
 fsqr_status fsqr_lambda_max(const fsqr_ctx* ctx, double* out_host) {
   if (!ctx || !out_host) return set_err(nullptr, FSQR_ERR_CONFIG, "null argument");
   for (int r = 0; r < ctx->R; ++r) out_host[r] = ctx->lambda_max[r];
@@ -1166,6 +1194,48 @@ fsqr_status fsqr_path_hbic(fsqr_ctx* ctx, double* hbic_host) {
   return FSQR_OK;
 }
 
+fsqr_status fsqr_tune(fsqr_ctx* ctx, const fsqr_tune_options* o, double* grid_host, double* hbic_host,
+                      int32_t* best_host, double* lam_piv_host, int64_t* total, void* stream) {
+  if (!ctx || !o || !best_host) return set_err(ctx, FSQR_ERR_CONFIG, "null argument");
+  if (o->T < 2 || !(o->lam_min_frac > 0.0 && o->lam_min_frac < 1.0) || o->B < 0 ||
+      (o->B > 0 && (!(o->alpha > 0.0 && o->alpha < 1.0) || !(o->c > 0.0))))
+    return set_err(ctx, FSQR_ERR_CONFIG, "fsqr_tune: need T >= 2, lam_min_frac in (0,1), B >= 0, alpha in (0,1), c > 0");
+  const int R = ctx->R, T = o->T;
+  std::vector<double> grid((size_t)R * T), piv(R, 0.0);
+  for (int r = 0; r < R; ++r) {
+    const double lmax = ctx->lambda_max[r];
+    double hi = lmax, lo = o->lam_min_frac * lmax;
+    if (o->B > 0) {
+      // pivotal lambda (reading R18): c times the ceil((1-alpha) B)-th order statistic of Lambda_b
+      std::vector<double> L((size_t)o->B);
+      fsqr_status s = fsqr_pivotal(ctx, r, o->B, o->seed, L.data(), stream);
+      if (s != FSQR_OK) return s;
+      std::sort(L.begin(), L.end());
+      const int64_t k = std::max<int64_t>(1, (int64_t)std::ceil((1.0 - o->alpha) * (double)o->B));
+      piv[r] = o->c * L[(size_t)(k - 1)];
+      hi = std::max(lmax, piv[r]);
+      lo = o->lam_min_frac * std::min(lmax, piv[r]);
+    }
+    // geometric grid hi -> lo (reading R20)
+    for (int t = 0; t < T; ++t) grid[(size_t)r * T + t] = hi * std::pow(lo / hi, (double)t / (double)(T - 1));
+  }
+  fsqr_status s = fsqr_path(ctx, grid.data(), T, total, nullptr, nullptr, nullptr, nullptr, nullptr, stream);
+  if (s != FSQR_OK) return s;
+  std::vector<double> h((size_t)R * T);
+  s = fsqr_path_hbic(ctx, h.data());
+  if (s != FSQR_OK) return s;
+  for (int r = 0; r < R; ++r) {
+    int b = 0;
+    for (int t = 1; t < T; ++t)
+      if (h[(size_t)r * T + t] < h[(size_t)r * T + b]) b = t;   // first minimal point
+    best_host[r] = b;
+  }
+  if (grid_host) memcpy(grid_host, grid.data(), sizeof(double) * grid.size());
+  if (hbic_host) memcpy(hbic_host, h.data(), sizeof(double) * h.size());
+  if (lam_piv_host) memcpy(lam_piv_host, piv.data(), sizeof(double) * R);
+  return FSQR_OK;
+}
+
 fsqr_status fsqr_path_beta(fsqr_ctx* ctx, int32_t r, int32_t t, int64_t cap, int64_t* idx_host, double* beta_host,
                            int64_t* count) {
   if (!ctx || !count) return set_err(ctx, FSQR_ERR_CONFIG, "null argument");
@@ -1227,7 +1297,7 @@ fsqr_status fsqr_profile_iterate(fsqr_ctx* ctx, int64_t k, double* stage_ms_host
     CK(cudaEventRecord(ev[3 * i + 1], st));
     launch_k1(D, ctx->k1_grid, st);
     CK(cudaEventRecord(ev[3 * i + 2], st));
-    launch_finalize(D, st);
+    if (!k1_fuses_finalize(D)) launch_finalize(D, st);   // else stage 3 is empty (fused into K1)
     CK(cudaEventRecord(ev[3 * i + 3], st));
   }
   CK(cudaGetLastError());

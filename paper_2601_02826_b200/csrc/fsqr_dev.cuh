@@ -72,7 +72,8 @@ struct Dev {
   int* sup_cnt;                     // [2]
   unsigned long long* cmax;         // [2][R] bits of max |beta_j/s_j|
   long long* sacc;                  // [R*n] int64 forward accumulators
-  long long* mterm;                 // [R]
+  long long* mterm;                 // [R] the colsum term of the forward sums
+  unsigned int* k1bar;              // [1] grid-barrier counter of k1_tcp's fused finalize
   // K2 partials + last-CTA ticket
   double* k2part;                   // [grid][R][FSQR_NPART]
   unsigned int* ticket;
@@ -496,6 +497,7 @@ void launch_k2_tc2(const Dev& D, const void* tmX, const void* tmB, int grid, cud
 cudaError_t k2_tc2_init();
 void launch_k2_simt(const Dev& D, int grid, cudaStream_t st);
 void launch_k1(const Dev& D, int grid, cudaStream_t st);
+bool k1_fuses_finalize(const Dev& D);   // the forward-product kernel also runs the finalize
 void launch_finalize(const Dev& D, cudaStream_t st);
 void launch_pack2(const uint8_t* x8, int64_t ld8, int n, int64_t p, uint8_t* x2, int64_t ld2, int* bad,
                   cudaStream_t st);

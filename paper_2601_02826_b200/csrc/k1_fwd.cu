@@ -437,6 +437,8 @@ void launch_k1_mode(const Dev& D, int grid, cudaStream_t st, int cur) {
 
 void launch_k1(const Dev& D, int grid, cudaStream_t st) { launch_k1_mode(D, grid, st, 0); }
 
+bool k1_fuses_finalize(const Dev& D) { return (D.k1_tc == 3 && D.storage == 2) || (D.k1_tc == 4 && D.storage == 1); }
+
 cudaError_t k1_init() {
   cudaError_t e;
   if ((e = init_r<1>()) != cudaSuccess) return e;

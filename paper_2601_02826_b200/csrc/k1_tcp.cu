@@ -25,10 +25,17 @@
 //   epilogue (converter warps): TMEM lane m of a row tile is row 16(m>>4) + 4(m&3) + ((m>>2)&3)
 //       scaled by 4^((m>>2)&3); each digit sum is shifted back exactly (a multiple of 4^q), then
 //       S = sum_k 256^k D_k in int64 and one 64-bit integer atomic per row and RHS, exactly the
-//       fixed-point sum k1_bulk forms (bit-identical results).
+//       fixed-point sum k1_bulk forms (bit-identical results);
+//   fused finalize (cur = 0): after its last item every CTA arrives at a grid barrier (the grid
+//       is one CTA per SM and fully co-resident: the next kernel is only launched once every CTA
+//       of this one has started, and nothing here waits on it); then the 256-row records of the
+//       n-vector step (fin_common.cuh: E15, residual, E12, theta digits) are spread over the CTAs,
+//       and the last CTA to finish them (ticket) reduces the records in fixed order and ends the
+//       iteration.  One launch instead of two.  (A first version let the last item of each row
+//       slab finalize that slab's 2048 rows: 8 records in one CTA put ~18 us on the tail.)
 #include <cuda.h>
 
-#include "fsqr_dev.cuh"
+#include "fin_common.cuh"
 
 #ifndef K1P_RTMAX
 #define K1P_RTMAX 16   // row tiles per slab cap (measurement knob)
@@ -175,7 +182,9 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
   const long long kit = *D.iter;
   const int par = (int)((kit + (cur ? 0 : 1)) & 1);
   const int cnt = D.sup_cnt[par];
-  const bool skip = *D.stop || cnt == 0 || (K1P_DBG & 16);
+  const bool stopped = *D.stop != 0;
+  const bool skip = stopped || cnt == 0 || (K1P_DBG & 16);
+  const bool fused = !cur;   // iteration mode: this kernel also runs the finalize (fin_common.cuh)
   const int R = D.R;
   const int nslab = (D.n + SR - 1) / SR;
   // entries per work item: about one item per CTA, at most 2^16 (int32 digit sums stay exact:
@@ -508,6 +517,59 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
   if (wid == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(T::TCOLS) : "memory");
+  }
+  if (!fused || stopped) return;
+
+  // ===================== fused finalize
+  // grid barrier: every CTA's forward sums (row atomics, colsum term) are complete and visible
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    atomicAdd(D.k1bar, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(D.k1bar) : "memory");
+    } while (v < gridDim.x);
+  }
+  __syncthreads();
+  // records (r, b) of the active RHS, contiguous shares per CTA, batches of <= 4 records of one RHS
+  // (warps 4..11 = one 256-thread group, named barrier 1; the A buffers are free scratch now)
+  double* smd = (double*)sA;
+  long long* smll = (long long*)(smd + 4 * 8 * 9);
+  const int nblk = (D.n + FG - 1) / FG;
+  if (wid >= 4) {
+    const int t = tid - 128;
+    const int tot = R * nblk, per = (tot + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int q0 = min(tot, (int)blockIdx.x * per), q1 = min(tot, q0 + per);
+    for (int q = q0; q < q1;) {
+      const int r = q / nblk, b = q % nblk, nb = min(min(4, nblk - b), q1 - q);
+      if (D.status[r] == ST_ACTIVE) {
+        const FinRHS c = fin_rhs(D, r, kit, __ldcg(D.mterm + r));
+        fin_records<4>(D, r, b, nb, c, t, 1, smd);
+      }
+      q += nb;
+    }
+  }
+  // ticket: the last CTA reduces every RHS's records in fixed order and ends the iteration
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(D.fticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last || wid < 4) return;
+  __threadfence();
+  const int t = tid - 128;
+  for (int r = 0; r < R; ++r) {
+    if (D.status[r] != ST_ACTIVE) continue;
+    const double b0v = D.beta[(int)(kit & 1)][r] + D.sumth[r] / D.eta[0];   // before fin_reduce_rhs rewrites sumth
+    grp_bar(1);
+    fin_reduce_rhs(D, r, nblk, b0v, kit, t, 1, smd, smll);
+    if (t == 0) D.mterm[r] = 0;
+  }
+  fin_iteration_tail(D, kit, t);
+  if (t == 0) {
+    *D.fticket = 0u;
+    *D.k1bar = 0u;   // every CTA has left the barrier (each took a ticket after it)
   }
 }
 

@@ -8,7 +8,7 @@
 //   R_p, R_z (w^{k+1}), loss, sum theta, and the digit planes of theta^{k+1}
 //   for the next X~^T theta pass.
 // Setup: column statistics (a0), power method pieces (a0'), lambda_max, state init.
-#include "fsqr_dev.cuh"
+#include "fin_common.cuh"
 
 namespace {
 
@@ -73,7 +73,6 @@ __device__ __forceinline__ double block_max(double v, double* sm) {
   return r;
 }
 
-__device__ __forceinline__ double rho_tau(double u, double tau) { return (tau - (u < 0.0 ? 1.0 : 0.0)) * u; }
 
 // theta -> balanced base-256 digit planes (rows 4r..4r+3 of Bq); returns sum T (exact)
 __device__ void quantize_theta(const Dev& D, int r, double mx, long long* smll) {
@@ -209,40 +208,15 @@ __global__ void __launch_bounds__(FT) k_finalize(const Dev D) {
 }
 
 // ---------------------------------------------------------------- multi-CTA finalize
-// Same arithmetic as k_finalize, one row per thread over ceil(n/256) CTAs.  Each CTA
-// quantises its rows of theta^{k+1} with the exponent of the previous iteration's
-// max|theta| (provisional); the last CTA to finish (ticket) reduces the partials in
-// CTA order, and only if the exponent of max|theta^{k+1}| differs does it
-// re-quantise every row, so the digit planes are always those of the exact rule
-// delta = 2^(e-28), e = exponent of max|theta^{k+1}| (as in quantize_theta).
-
-__device__ __forceinline__ long long quant_row(const Dev& D, int r, int i, double th, double inv) {
-  long long T = isfinite(th) ? __double2ll_rn(th * inv) : 0;
-  const long long Tr = T;
-  int8_t* b0 = D.Bq + (int64_t)(4 * r) * D.ldk;
-  const int d3 = (int)(int8_t)(T & 0xFF);
-  T = (T - d3) >> 8;
-  const int d2 = (int)(int8_t)(T & 0xFF);
-  T = (T - d2) >> 8;
-  const int d1 = (int)(int8_t)(T & 0xFF);
-  T = (T - d1) >> 8;
-  const int ix = bq_index(D, i);
-  b0[ix] = (int8_t)T;
-  b0[D.ldk + ix] = (int8_t)d1;
-  b0[2 * D.ldk + ix] = (int8_t)d2;
-  b0[3 * D.ldk + ix] = (int8_t)d3;
-  return Tr;
-}
-
-__device__ __forceinline__ int theta_exponent(double mx) {
-  int ex = 0;
-  if (mx > 0.0 && isfinite(mx)) frexp(mx, &ex);
-  return ex;
-}
+// The n-vector step after the CUDA-core forward product (k1_bulk; the tensor-core forward product
+// k1_tcp runs the same records in its own tail, fin_common.cuh).  Grid (ceil(n/256), R): CTA
+// (x, r) computes record x of RHS r (rows 256x.., one row per thread), quantising theta^{k+1}
+// provisionally with the previous exponent; the last CTA of RHS r (ticket fticket[1 + r]) reduces
+// its records in order and re-quantises only on a binade change; the last CTA overall runs the
+// iteration tail.
 
 __global__ void __launch_bounds__(FIN_THREADS) k_finalize_mc(const Dev D) {
-  // grid (ceil(n/256), R): CTA (x, r) owns rows 256x.. of RHS r.  Tickets: fticket[1 + r] elects the
-  // last CTA of RHS r (its fixed-order reduction), fticket[0] the last CTA overall (iteration tail).
+  static_assert(FIN_THREADS == FG, "one record per CTA");
   __shared__ double smd[32 * 8 + 8];
   __shared__ long long smll[33];
   __shared__ bool s_last;
@@ -250,110 +224,25 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize_mc(const Dev D) {
   pdl_wait();
   if (*D.stop) return;
   const long long k = *D.iter;
-  const int par = (int)(k & 1), par1 = par ^ 1;
-  const int n = D.n;
-  const int r = blockIdx.y;
-  const int i = blockIdx.x * FIN_THREADS + threadIdx.x;
+  const int r = blockIdx.y, t = threadIdx.x;
   const int nblk = gridDim.x;
   if (D.status[r] == ST_ACTIVE) {
-    const double b0 = D.beta[par][r] + D.sumth[r] / D.eta[0];   // E14 with lambda_0 = 0, g_0 = sum theta^k
-    const double tau = D.tau[r];
-    const double mu = D.mu, sig = D.sigma;
-    const double tn = tau / ((double)n * mu), un = (1.0 - tau) / ((double)n * mu);
-    const int cnt = D.sup_cnt[par1];
-    const double cm = __longlong_as_double((long long)D.cmax[par1 * D.R + r]);
-    const int E = fwd_exponent(cm, cnt, n);
-    const long long mt = D.mterm[r];
-    const double inv_scale = ldexp(1.0, -E);
-    const double inv_prev = 1.0 / D.delta[r];   // 1/delta^k, exact (a power of two)
-    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    long long ts = 0;
-    if (i < n) {
-      const int64_t o = (int64_t)r * n + i;
-      const double sv = (double)((long long)n * D.sacc[o] - mt) * inv_scale / (double)n + b0;
-      D.sacc[o] = 0;
-      const double yi = D.y[i];
-      const double zo = D.z[o], th = D.theta[o], ro = D.rres[o];
-      const double zn = pos_part(zo + th / mu - tn) - pos_part(-zo - th / mu - un);   // E15
-      const double rn = sv + zn - yi;
-      const double thn = th - sig * (2.0 * rn - ro);                                  // E12
-      D.z[o] = zn;
-      D.theta[o] = thn;
-      D.rres[o] = rn;
-      D.s[o] = sv;
-      const double nt = (double)n * thn;
-      const double dz = zn - prox_rho1(zn + nt, tau);
-      acc[0] = rn * rn;
-      acc[1] = zn * zn;
-      acc[2] = nt * nt;
-      acc[3] = dz * dz;
-      acc[4] = rho_tau(yi - sv, tau);
-      acc[5] = thn;
-      acc[6] = yi * yi;
-      acc[7] = isfinite(thn) ? fabs(thn) : thn;
-      ts = quant_row(D, r, i, thn, inv_prev);
-    }
-    block_sum<7>(*(double(*)[7])acc, smd);
-    const double mxb = block_max(acc[7], smd);
-    ts = block_sum_ll(ts, smll);
-    if (threadIdx.x == 0) {
-      double* fp = D.fpart + ((size_t)blockIdx.x * D.R + r) * FSQR_FPART;
-      for (int q = 0; q < 7; ++q) fp[q] = acc[q];
-      fp[7] = mxb;
-      D.ftsum[(size_t)blockIdx.x * D.R + r] = ts;
-    }
+    const FinRHS c = fin_rhs(D, r, k, D.mterm[r]);
+    fin_records<1>(D, r, blockIdx.x, 1, c, t, 0, smd);
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(D.fticket + 1 + r, 1u) == (unsigned)nblk - 1;
+    if (t == 0) s_last = atomicAdd(D.fticket + 1 + r, 1u) == (unsigned)nblk - 1;
     __syncthreads();
     if (s_last) {
       __threadfence();
-      // ---------------------------------------- last CTA of RHS r: fixed-order reduction over its CTAs
-      __shared__ double s_dlt;
-      __shared__ int s_requant;
-      double a[7];
-      reduce_records<7>(D.fpart + (size_t)r * FSQR_FPART, nblk, D.R * FSQR_FPART, a, smd);
-      double mxl = 0.0;
-      long long tsl = 0;
-      for (int b = threadIdx.x; b < nblk; b += FIN_THREADS) {
-        const double m = D.fpart[((size_t)b * D.R + r) * FSQR_FPART + 7];
-        mxl = (m > mxl || !isfinite(m)) ? m : mxl;
-        tsl += D.ftsum[(size_t)b * D.R + r];
-      }
-      const double mx = block_max(mxl, smd);
-      const long long tsum = block_sum_ll(tsl, smll);
-      if (threadIdx.x == 0) {
-        double* sc = D.scal + r * FSQR_NSCAL;
-        sc[0] = sqrt(a[0]) / (1.0 + sqrt(a[6]));
-        sc[1] = sqrt(a[3]) / (1.0 + sqrt(a[1]) + sqrt(a[2]));
-        sc[2] = a[4];
-        sc[3] = a[6];
-        D.beta[par1][r] = b0;
-        D.sumth[r] = a[5];
+      fin_reduce_rhs(D, r, nblk, c.b0, k, t, 0, smd, smll);
+      if (t == 0) {
         D.mterm[r] = 0;
-        const int e_new = theta_exponent(mx);
-        const int e_old = theta_exponent(D.delta[r] * ldexp(1.0, 28) * 0.75);   // delta^k = 2^(e_old - 28)
-        s_requant = (e_new != e_old) ? 1 : 0;
-        const double dlt = (mx > 0.0 && isfinite(mx)) ? ldexp(1.0, e_new - 28) : 1.0;
-        s_dlt = dlt;
-        if (!s_requant) D.Tsum[r] = tsum;
-        D.delta[r] = dlt;
         D.fticket[1 + r] = 0u;
       }
-      __syncthreads();
-      if (s_requant) {
-        const double inv = 1.0 / s_dlt;
-        long long t2 = 0;
-        for (int ii = threadIdx.x; ii < n; ii += FIN_THREADS) t2 += quant_row(D, r, ii, D.theta[(int64_t)r * n + ii], inv);
-        t2 = block_sum_ll(t2, smll);
-        if (threadIdx.x == 0) D.Tsum[r] = t2;
-      }
       if (D.R == 1) {   // one RHS: its last CTA is the last CTA overall, no second ticket round
-        if (threadIdx.x == 0) {
-          D.cmax[par] = 0ull;
-          D.sup_cnt[par] = 0;
-          *D.iter = k + 1;
-        }
+        fin_iteration_tail(D, k, t);
+        return;
       }
     }
     if (D.R == 1) return;
@@ -361,19 +250,12 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize_mc(const Dev D) {
   // ------------------------------------------------ last CTA overall: iteration tail
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(D.fticket, 1u) == (unsigned)(nblk * D.R) - 1;
+  if (t == 0) s_last = atomicAdd(D.fticket, 1u) == (unsigned)(nblk * D.R) - 1;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  if (threadIdx.x < D.R) {
-    D.cmax[par * D.R + threadIdx.x] = 0ull;
-    if (D.status[threadIdx.x] == ST_SWITCH) D.status[threadIdx.x] = ST_ACTIVE;   // re-test w^k at lambda_{t+1}
-  }
-  if (threadIdx.x == 0) {
-    D.sup_cnt[par] = 0;
-    *D.iter = k + 1;
-    *D.fticket = 0u;
-  }
+  fin_iteration_tail(D, k, t);
+  if (t == 0) *D.fticket = 0u;
 }
 
 // state init after create / set_state: s from the support list of the current parity (k1 in cur mode)

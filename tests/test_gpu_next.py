@@ -161,3 +161,31 @@ def test_path_hbic_and_tune_match_oracle(cuda_ok):
     np.testing.assert_allclose(out["hbic"][0], ho, rtol=1e-6)
     assert out["best"][0] == int(np.argmin(ho))
     assert rel(out["beta"][0], o["beta_path"][int(np.argmin(ho))]) < 1e-4
+
+
+def test_tune_with_pivotal_grid(cuda_ok):
+    """fsqr_tune with B > 0 (reading R20): lambda_piv = 1.1 x the ceil(0.9 B)-th order statistic of
+    the pivotal statistic (reading R18; equal to the oracle's), the grid runs geometrically from
+    max(lambda_max, lambda_piv) to lam_min_frac x min(lambda_max, lambda_piv), and HBIC of every
+    point equals the oracle's HBIC of the oracle path on the same grid."""
+    import paper_2601_02826_b200 as fs
+
+    prob = datagen.make("c2", n=500, p=1500)
+    d = oracle.Design.from_problem(prob)
+    tau, G, T, tol, B, frac = 0.5, 5, 6, 1e-5, 256, 0.2
+    mu = 2.0 / prob.n
+    eta = oracle.eta(d, G, mu)
+    X, y = to_device(prob)
+    S = fs.Solver(X, prob.storage, prob.n, prob.p, prob.ld, y, [tau], [1.0], G=G, mu=mu, eta=eta, tol=tol,
+                  max_iter_point=5000)
+    out = S.tune(T=T, lam_min_frac=frac, B=B, seed=99)
+    lpiv = oracle.pivotal_lambda(oracle.pivotal(d, tau, B, seed=99), alpha=0.1, c=1.1)
+    assert out["lam_piv"][0] == pytest.approx(lpiv, rel=1e-10)
+    lm = oracle.lambda_max(d, prob.y, tau)[0]
+    hi, lo = max(lm, lpiv), frac * min(lm, lpiv)
+    np.testing.assert_allclose(out["grid"][0], hi * (lo / hi) ** (np.arange(T) / (T - 1)), rtol=1e-12)
+    o = oracle.path(d, prob.y, tau, out["grid"][0], eta, mu, G, tol, 5000)
+    ho = np.array([oracle.hbic(d, prob.y, tau, o["beta_path"][t]) for t in range(T)])
+    np.testing.assert_allclose(out["hbic"][0], ho, rtol=1e-6)
+    assert out["best"][0] == int(np.argmin(ho))
+    assert rel(out["beta"][0], o["beta_path"][int(np.argmin(ho))]) < 1e-6

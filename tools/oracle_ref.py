@@ -53,9 +53,23 @@ def design_checksum(prob) -> str:
 
 
 def lam_frac(name: str, prob) -> float:
-    if name == "c5":
-        return prob.lam_min_frac ** (C5_POINT / (prob.path_points - 1))
+    if name == "c5":   # the C5 recipe's path (the M instance shares the design but has no path)
+        cfg = datagen.CONFIGS["c5"]
+        return cfg["lam_min"] ** (C5_POINT / (cfg["path"] - 1))
     return prob.lam_frac
+
+
+def cached_eta(name: str, cks: str):
+    """eta of an earlier run of this script on the same design (M and C5 share it), else None."""
+    key = ("m", "c5") if name in ("m", "c5") else (name,)
+    if not os.path.isdir(OUT):
+        return None
+    for fn in sorted(os.listdir(OUT)):
+        if fn.split("_tau")[0] in key:
+            z = np.load(os.path.join(OUT, fn))
+            if json.loads(str(z["meta"]))["checksum"] == cks:
+                return z["eta"]
+    return None
 
 
 def run(name: str, iters: int, prob=None, d=None, eta=None, log=print):
@@ -67,6 +81,8 @@ def run(name: str, iters: int, prob=None, d=None, eta=None, log=print):
     cks = design_checksum(prob)
     mu, G = 2.0 / prob.n, prob.G
     t_eta = 0.0
+    if eta is None:
+        eta = cached_eta(name, cks)
     if eta is None:
         t0 = time.perf_counter()
         eta = oracle.eta(d, G, mu)
