@@ -289,6 +289,11 @@ fsqr_status fsqr_trace(fsqr_ctx* ctx, double* out_host, int64_t cap_rows, int64_
  * the total (first to last event).  Blocking. */
 fsqr_status fsqr_profile_iterate(fsqr_ctx* ctx, int64_t k, double* stage_ms_host, double* total_ms_host, void* stream);
 
+/* Measurement builds only (compile-time instrumentation, tools/k1_timing.py): copies up to n of the
+ * per-CTA %globaltimer stamps the instrumented kernels wrote for one iteration; all zero in the
+ * shipped build.  Waits for the device. */
+fsqr_status fsqr_debug_stamps(fsqr_ctx* ctx, uint64_t* out_host, int64_t n);
+
 /* total outer iterations since create/set_state (device counter; synchronises). */
 int64_t fsqr_iterations(fsqr_ctx* ctx);
 

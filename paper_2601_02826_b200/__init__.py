@@ -65,7 +65,7 @@ EXPORTS = ["fsqr_default_options", "fsqr_create", "fsqr_iterate", "fsqr_solve", 
            "fsqr_get_beta", "fsqr_get_state", "fsqr_set_state", "fsqr_set_lambda", "fsqr_lambda_max",
            "fsqr_get_eta", "fsqr_get_colstats", "fsqr_path", "fsqr_path_beta", "fsqr_trace", "fsqr_iterations",
            "fsqr_profile_iterate", "fsqr_hbic", "fsqr_set_lambda_weights", "fsqr_lla", "fsqr_pivotal", "fsqr_set_lambda2", "fsqr_path_hbic",
-           "fsqr_tune", "fsqr_set_tolerance", "fsqr_launches_per_iteration", "fsqr_backend_name", "fsqr_fit_host", "fsqr_pack2", "fsqr_last_error", "fsqr_global_error", "fsqr_status_str",
+           "fsqr_tune", "fsqr_set_tolerance", "fsqr_launches_per_iteration", "fsqr_debug_stamps", "fsqr_backend_name", "fsqr_fit_host", "fsqr_pack2", "fsqr_last_error", "fsqr_global_error", "fsqr_status_str",
            "fsqr_destroy"]
 
 
@@ -117,6 +117,7 @@ def load(build_if_missing: bool = True):
     L.fsqr_set_lambda_weights.argtypes = [ctxp, P, P]
     L.fsqr_lla.argtypes = [ctxp, I32, D, I32, P, ctypes.POINTER(fsqr_result), P]
     L.fsqr_set_tolerance.argtypes = [ctxp, D, I64]
+    L.fsqr_debug_stamps.argtypes = [ctxp, P, I64]
     L.fsqr_launches_per_iteration.argtypes = [ctxp]
     L.fsqr_launches_per_iteration.restype = I32
     L.fsqr_iterations.argtypes = [ctxp]
@@ -138,7 +139,7 @@ def load(build_if_missing: bool = True):
                  "fsqr_get_state", "fsqr_set_state", "fsqr_set_lambda", "fsqr_lambda_max", "fsqr_get_eta",
                  "fsqr_get_colstats", "fsqr_path", "fsqr_path_beta", "fsqr_trace", "fsqr_fit_host", "fsqr_hbic",
                  "fsqr_set_lambda_weights", "fsqr_lla", "fsqr_pivotal", "fsqr_set_lambda2", "fsqr_path_hbic", "fsqr_pack2",
-                 "fsqr_tune", "fsqr_set_tolerance"):
+                 "fsqr_tune", "fsqr_set_tolerance", "fsqr_debug_stamps"):
         getattr(L, name).restype = S
     _lib = L
     return L
@@ -363,6 +364,12 @@ def fsqr_pivotal(ctx, rhs: int, B: int, seed: int = 0x5EED, stream=None) -> np.n
 
 def fsqr_set_tolerance(ctx, tol: float, max_iter: int):
     return _check(load().fsqr_set_tolerance(ctx, float(tol), int(max_iter)), ctx)
+
+
+def fsqr_debug_stamps(ctx, n: int = 2048) -> np.ndarray:
+    out = np.zeros(n, dtype=np.uint64)
+    _check(load().fsqr_debug_stamps(ctx, _ptr(out), n), ctx)
+    return out
 
 
 def fsqr_launches_per_iteration(ctx) -> int:

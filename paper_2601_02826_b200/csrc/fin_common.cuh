@@ -10,12 +10,14 @@
 //   sum theta, ||y||^2, max|theta| (reading R1), and the int8 digit planes of theta^{k+1}.
 //
 // Unit of work: a RECORD = 256 consecutive rows of one RHS, computed by a group of 256 threads
-// (one row per thread, named barrier).  Records are reduced in a fixed order by a group of 256
-// threads, so the result is bitwise the same whichever kernel computed the records.
+// (one row per thread, named barrier).  Records are reduced in a fixed order (fin_reduce_warp), so
+// the result is bitwise the same whichever kernel computed the records.
 #pragma once
 #include "fsqr_dev.cuh"
 
 constexpr int FG = 256;   // threads per finalize group = rows per record
+
+
 
 __device__ __forceinline__ void grp_bar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(FG) : "memory"); }
 
@@ -81,19 +83,6 @@ __device__ __forceinline__ double grp_max(double v, double* sm, int t, int bar) 
   return r;
 }
 
-// fixed-order sum of NV values over `count` records (record b at base + b * stride): thread t adds
-// records t, t + 256, ... in order, then grp_sum's tree.  sm: 32 * NV + NV doubles.
-template <int NV>
-__device__ __forceinline__ void grp_reduce_records(const double* base, int count, int stride, double (&out)[NV],
-                                                   double* sm, int t, int bar) {
-#pragma unroll
-  for (int q = 0; q < NV; ++q) out[q] = 0.0;
-  for (int b = t; b < count; b += FG)
-#pragma unroll
-    for (int q = 0; q < NV; ++q) out[q] += __ldcg(base + (size_t)b * stride + q);
-  grp_sum<NV>(out, sm, t, bar);
-}
-
 __device__ __forceinline__ double rho_tau(double u, double tau) { return (tau - (u < 0.0 ? 1.0 : 0.0)) * u; }
 
 // theta_i -> T = round(theta_i / delta) and its balanced base-256 digits in rows 4r..4r+3 of Bq
@@ -143,37 +132,57 @@ __device__ __forceinline__ FinRHS fin_rhs(const Dev& D, int r, long long k, long
   return c;
 }
 
-// Records b0 .. b0 + nb - 1 (nb <= NB) of RHS r, thread t taking row 256 (b0 + q) + t of each:
-// every row's loads are issued before any of its arithmetic (one memory latency per batch, not
-// per record).  Each record is reduced the same way wherever it is computed: a butterfly within
-// each warp, then the 8 warp sums added in warp order (max and int64 alike).  Writes
-// fpart[b][r][0..7] and ftsum[b][r].  sm: NB * 8 * 9 doubles.  Group-wide call.
+// The state rows a record batch reads that do not depend on this iteration's forward product
+// (z^k, theta^k, r^k, y): loaded before the forward sums are complete (fin_load), so that after
+// them only the accumulators remain on the critical path.
 template <int NB>
-__device__ __forceinline__ void fin_records(const Dev& D, int r, int b0, int nb, const FinRHS& c, int t, int bar,
-                                            double* sm) {
-  const int n = D.n, lane = t & 31, wid = t >> 5;
-  const double mu = D.mu, sig = D.sigma;
-  double sa[NB], zo[NB], th[NB], ro[NB], yi[NB];
+struct FinRows {
+  double zo[NB], th[NB], ro[NB], yi[NB];
+};
+
+template <int NB>
+__device__ __forceinline__ void fin_load(const Dev& D, int r, int b0, int nb, int t, FinRows<NB>& w) {
+  const int n = D.n;
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
     const int i = (b0 + q) * FG + t;
     const bool ok = q < nb && i < n;
     const int64_t o = (int64_t)r * n + i;
-    sa[q] = ok ? (double)((long long)n * __ldcg(D.sacc + o) - c.mt) : 0.0;
-    zo[q] = ok ? D.z[o] : 0.0;
-    th[q] = ok ? D.theta[o] : 0.0;
-    ro[q] = ok ? D.rres[o] : 0.0;
-    yi[q] = ok ? D.y[i] : 0.0;
+    w.zo[q] = ok ? D.z[o] : 0.0;
+    w.th[q] = ok ? D.theta[o] : 0.0;
+    w.ro[q] = ok ? D.rres[o] : 0.0;
+    w.yi[q] = ok ? D.y[i] : 0.0;
   }
+}
+
+// Records b0 .. b0 + nb - 1 (nb <= NB) of RHS r, thread t taking row 256 (b0 + q) + t of each
+// (rows pre-loaded by fin_load).  Each record is reduced the same way wherever it is computed: a
+// butterfly within each warp, then the 8 warp sums added in warp order (max and int64 alike).
+// Writes fpart[b][r][0..7] and ftsum[b][r].  sm: NB * 8 * 9 doubles.  Group-wide call.
+template <int NB>
+__device__ __forceinline__ void fin_records(const Dev& D, int r, int b0, int nb, const FinRHS& c, int t, int bar,
+                                            double* sm, const FinRows<NB>& w) {
+  const int n = D.n, lane = t & 31, wid = t >> 5;
+  const double mu = D.mu, sig = D.sigma;
+  double sa[NB];
+  const double *zo = w.zo, *th = w.th, *ro = w.ro, *yi = w.yi;
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
     const int i = (b0 + q) * FG + t;
-    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    long long ts = 0;
+    const bool ok = q < nb && i < n;
+    sa[q] = ok ? (double)((long long)n * __ldcg(D.sacc + (int64_t)r * n + i) - c.mt) : 0.0;
+  }
+  double acc[NB][8];
+  long long ts[NB];
+#pragma unroll
+  for (int q = 0; q < NB; ++q) {
+    const int i = (b0 + q) * FG + t;
+#pragma unroll
+    for (int v = 0; v < 8; ++v) acc[q][v] = 0.0;
+    ts[q] = 0;
     if (q < nb && i < n) {
       const int64_t o = (int64_t)r * n + i;
       const double sv = sa[q] * c.inv_scale / (double)n + c.b0;
-      D.sacc[o] = 0;
       const double zn = pos_part(zo[q] + th[q] / mu - c.tn) - pos_part(-zo[q] - th[q] / mu - c.un);   // E15
       const double rn = sv + zn - yi[q];
       const double thn = th[q] - sig * (2.0 * rn - ro[q]);                                             // E12
@@ -183,29 +192,36 @@ __device__ __forceinline__ void fin_records(const Dev& D, int r, int b0, int nb,
       D.s[o] = sv;
       const double nt = (double)n * thn;
       const double dz = zn - prox_rho1(zn + nt, c.tau);
-      acc[0] = rn * rn;
-      acc[1] = zn * zn;
-      acc[2] = nt * nt;
-      acc[3] = dz * dz;
-      acc[4] = rho_tau(yi[q] - sv, c.tau);
-      acc[5] = thn;
-      acc[6] = yi[q] * yi[q];
-      acc[7] = isfinite(thn) ? fabs(thn) : thn;
-      ts = quant_row(D, r, i, thn, c.inv_prev);   // provisional: the exponent of delta^k
+      acc[q][0] = rn * rn;
+      acc[q][1] = zn * zn;
+      acc[q][2] = nt * nt;
+      acc[q][3] = dz * dz;
+      acc[q][4] = rho_tau(yi[q] - sv, c.tau);
+      acc[q][5] = thn;
+      acc[q][6] = yi[q] * yi[q];
+      acc[q][7] = isfinite(thn) ? fabs(thn) : thn;
+      ts[q] = quant_row(D, r, i, thn, c.inv_prev);   // provisional: the exponent of delta^k
     }
-    // warp level (lane 0 holds the warp's values)
+  }
+  // warp level, all records and values interleaved level by level (the same butterfly per value as
+  // warp_sum_d; lane 0 ends with the warp's values)
 #pragma unroll
-    for (int v = 0; v < 7; ++v) acc[v] = warp_sum_d(acc[v]);
+  for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      acc[7] = fmax(acc[7], __shfl_xor_sync(0xffffffffu, acc[7], o));
-      ts += __shfl_xor_sync(0xffffffffu, ts, o);
+    for (int q = 0; q < NB; ++q) {
+#pragma unroll
+      for (int v = 0; v < 7; ++v) acc[q][v] += __shfl_xor_sync(0xffffffffu, acc[q][v], o);
+      acc[q][7] = fmax(acc[q][7], __shfl_xor_sync(0xffffffffu, acc[q][7], o));
+      ts[q] += __shfl_xor_sync(0xffffffffu, ts[q], o);
     }
-    if (lane == 0) {
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
       double* w = sm + (q * 8 + wid) * 9;
 #pragma unroll
-      for (int v = 0; v < 8; ++v) w[v] = acc[v];
-      w[8] = __longlong_as_double(ts);
+      for (int v = 0; v < 8; ++v) w[v] = acc[q][v];
+      w[8] = __longlong_as_double(ts[q]);
     }
   }
   grp_bar(bar);
@@ -234,47 +250,82 @@ __device__ __forceinline__ void fin_records(const Dev& D, int r, int b0, int nb,
 // All nblk records of RHS r are written: reduce them in record order, publish R_p, R_z, the loss
 // and sum theta^{k+1}, beta_0^{k+1}, and fix the digit planes if max|theta^{k+1}| left the binade
 // of delta^k (then every row is re-quantised with delta^{k+1} = 2^(e-28)).  Group-wide call.
-__device__ __forceinline__ void fin_reduce_rhs(const Dev& D, int r, int nblk, double b0, long long k, int t, int bar,
-                                               double* smd, long long* smll) {
-  __shared__ double s_dlt;
-  __shared__ int s_requant;
-  const int n = D.n;
-  double a[7];
-  grp_reduce_records<7>(D.fpart + (size_t)r * FSQR_FPART, nblk, D.R * FSQR_FPART, a, smd, t, bar);
-  double mxl = 0.0;
-  long long tsl = 0;
-  for (int b = t; b < nblk; b += FG) {
-    const double m = __ldcg(D.fpart + ((size_t)b * D.R + r) * FSQR_FPART + 7);
-    mxl = (m > mxl || !isfinite(m)) ? m : mxl;
-    tsl += __ldcg(D.ftsum + (size_t)b * D.R + r);
+// All nblk records of RHS r are written: ONE WARP reduces them in record order (lane l adds records
+// l, l + 32, ..., all nine values of a record in one round of loads; then a level-major butterfly),
+// and lane 0 publishes R_p, R_z, the loss and sum theta^{k+1}, beta_0^{k+1} and delta^{k+1}.
+// Returns (on every lane) whether max|theta^{k+1}| left the binade of delta^k: then every row must
+// be re-quantised with delta^{k+1} = 2^(e-28) (fin_requant).  Several RHS reduce on different warps.
+__device__ __forceinline__ bool fin_reduce_warp(const Dev& D, int r, int nblk, double b0, long long k, int lane) {
+  double a[7] = {0, 0, 0, 0, 0, 0, 0};
+  double mx = 0.0;
+  long long tsum = 0;
+  for (int b = lane; b < nblk; b += 32) {
+    const double* fp = D.fpart + ((size_t)b * D.R + r) * FSQR_FPART;
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = __ldcg(fp + q);
+    const long long ts = __ldcg(D.ftsum + (size_t)b * D.R + r);
+#pragma unroll
+    for (int q = 0; q < 7; ++q) a[q] += v[q];
+    mx = (v[7] > mx || !isfinite(v[7])) ? v[7] : mx;
+    tsum += ts;
   }
-  const double mx = grp_max(mxl, smd, t, bar);
-  const long long tsum = grp_sum_ll(tsl, smll, t, bar);
-  if (t == 0) {
+  const double dprev = D.delta[r];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int q = 0; q < 7; ++q) a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
+    const double m = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = (m > mx || !isfinite(m)) ? m : mx;
+    tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
+  }
+  const int e_new = theta_exponent(mx);
+  const int e_old = theta_exponent(dprev * ldexp(1.0, 28) * 0.75);   // delta^k = 2^(e_old - 28)
+  const bool requant = e_new != e_old;
+  const double rp = sqrt(a[0]) / (1.0 + sqrt(a[6]));
+  const double rz = sqrt(a[3]) / (1.0 + sqrt(a[1]) + sqrt(a[2]));
+  const double dnew = (mx > 0.0 && isfinite(mx)) ? ldexp(1.0, e_new - 28) : 1.0;
+  if (lane == 0) {
     double* sc = D.scal + r * FSQR_NSCAL;
-    sc[0] = sqrt(a[0]) / (1.0 + sqrt(a[6]));
-    sc[1] = sqrt(a[3]) / (1.0 + sqrt(a[1]) + sqrt(a[2]));
+    sc[0] = rp;
+    sc[1] = rz;
     sc[2] = a[4];
     sc[3] = a[6];
     D.beta[(int)(k & 1) ^ 1][r] = b0;
     D.sumth[r] = a[5];
-    const int e_new = theta_exponent(mx);
-    const int e_old = theta_exponent(D.delta[r] * ldexp(1.0, 28) * 0.75);   // delta^k = 2^(e_old - 28)
-    s_requant = (e_new != e_old) ? 1 : 0;
-    const double dlt = (mx > 0.0 && isfinite(mx)) ? ldexp(1.0, e_new - 28) : 1.0;
-    s_dlt = dlt;
-    if (!s_requant) D.Tsum[r] = tsum;
-    D.delta[r] = dlt;
+    if (!requant) D.Tsum[r] = tsum;
+    D.delta[r] = dnew;
+  }
+  return requant;
+}
+
+// re-quantise every row of RHS r with delta^{k+1} (already published); group-wide call
+__device__ __forceinline__ void fin_requant(const Dev& D, int r, int t, int bar, long long* smll) {
+  const int n = D.n;
+  const double inv = 1.0 / D.delta[r];
+  long long t2 = 0;
+  for (int ii = t; ii < n; ii += FG) t2 += quant_row(D, r, ii, D.theta[(int64_t)r * n + ii], inv);
+  t2 = grp_sum_ll(t2, smll, t, bar);
+  if (t == 0) D.Tsum[r] = t2;
+  grp_bar(bar);
+}
+
+// every active RHS's records: warp w of the group reduces RHS w, w + 8, ...; then the rare
+// re-quantisations, group-wide.  b0 per RHS from the state before this call (beta^k, sum theta^k).
+__device__ __forceinline__ void fin_reduce_all(const Dev& D, int nblk, long long k, int t, int bar, long long* smll) {
+  __shared__ unsigned s_req;
+  const int lane = t & 31, wid = t >> 5;
+  if (t == 0) s_req = 0u;
+  grp_bar(bar);
+  for (int r = wid; r < D.R; r += FG / 32) {
+    if (D.status[r] != ST_ACTIVE) continue;
+    const double b0 = D.beta[(int)(k & 1)][r] + D.sumth[r] / D.eta[0];   // E14 with lambda_0 = 0, g_0 = sum theta^k
+    if (fin_reduce_warp(D, r, nblk, b0, k, lane) && lane == 0) atomicOr(&s_req, 1u << r);
   }
   grp_bar(bar);
-  if (s_requant) {
-    const double inv = 1.0 / s_dlt;
-    long long t2 = 0;
-    for (int ii = t; ii < n; ii += FG) t2 += quant_row(D, r, ii, D.theta[(int64_t)r * n + ii], inv);
-    t2 = grp_sum_ll(t2, smll, t, bar);
-    if (t == 0) D.Tsum[r] = t2;
-  }
-  grp_bar(bar);
+  const unsigned req = s_req;
+  for (int r = 0; r < D.R; ++r)
+    if (req & (1u << r)) fin_requant(D, r, t, bar, smll);
 }
 
 // iteration tail (after every RHS is reduced): clear the forward scale and support count of the

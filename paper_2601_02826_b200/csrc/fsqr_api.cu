@@ -532,17 +532,63 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
   if (D.k1_tc == 3 || D.k1_tc == 4) CK(k1_tcp_init());
 
   // ---------------- allocations
+  // Everything the n-vector step and the per-iteration control touch (n-vectors, theta digits,
+  // finalize records, scalars, tickets) lives in ONE arena: measured on the B200, the first
+  // accesses of the tail to a dozen separate small allocations right after the 2.5 GB X stream
+  // stalled up to 8 us (address-translation misses); one contiguous block needs few translations.
   int32_t* colsum;
   double *mean, *inv_sd, *sd, *eta_d, *inv_eta_d, *y, *tau_d, *lam_cur;
   AL(colsum, X->p);
   AL(mean, X->p);
   AL(inv_sd, X->p);
   AL(sd, X->p);
-  AL(eta_d, o.G);
-  AL(inv_eta_d, o.G);
-  AL(y, X->n);
-  AL(tau_d, R);
-  AL(lam_cur, R);
+  {
+    std::vector<std::pair<void**, size_t>> req;
+    auto add = [&](auto** ptr, size_t count) { req.push_back({(void**)ptr, count * sizeof(**ptr)}); };
+    add(&y, X->n);
+    add(&D.z, nR);
+    add(&D.theta, nR);
+    add(&D.rres, nR);
+    add(&D.s, nR);
+    add(&D.sdense, nR);
+    add(&D.sacc, nR);
+    add(&D.Bq, (size_t)D.npad * D.ldk);
+    add(&D.fpart, (size_t)FIN_MAXGRID * R * FSQR_FPART);
+    add(&D.ftsum, (size_t)FIN_MAXGRID * R);
+    add(&D.k2part, (size_t)std::max(ctx->k2_grid, ctx->sms * 8) * R * FSQR_NPART);
+    add(&eta_d, o.G);
+    add(&inv_eta_d, o.G);
+    add(&tau_d, R);
+    add(&lam_cur, R);
+    add(&D.lam2, R);
+    add(&D.use_w, 1);
+    add(&D.Tsum, R);
+    add(&D.delta, R);
+    add(&D.sumth, R);
+    add(&D.sup_cnt, 2);
+    add(&D.cmax, 2 * R);
+    add(&D.mterm, R);
+    add(&D.k1bar, 1);
+    add(&D.ticket, 1);
+    add(&D.kbase, 1);
+    add(&D.fticket, 1 + FSQR_MAXR);
+    add(&D.scal, R * FSQR_NSCAL);
+    add(&D.status, R);
+    add(&D.commit_iter, R);
+    add(&D.iter, 1);
+    add(&D.stop, 1);
+    add(&D.lastR, R * FSQR_TRACE_W);
+    add(&D.t_idx, R);
+    add(&D.pt_iters, R);
+    size_t total = 0;
+    for (auto& q : req) total += (q.second + 255) / 256 * 256;
+    uint8_t* arena;
+    AL(arena, total);
+    for (auto& q : req) {
+      *q.first = arena;
+      arena += (q.second + 255) / 256 * 256;
+    }
+  }
   D.colsum = colsum;
   D.mean = mean;
   D.inv_sd = inv_sd;
@@ -552,9 +598,7 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
   D.tau = tau_d;
   D.lam_cur = lam_cur;
   // penalty weights: ctx-owned [(p+1)][R]; the caller's [p+1] vector (if any) is broadcast to every RHS
-  AL(D.lam2, R);
   AL(D.lamw, p1 * R);
-  AL(D.use_w, 1);
   if (lamw_dev) {
     for (int r = 0; r < R; ++r)
       CK(cudaMemcpy2DAsync(D.lamw + r, sizeof(double) * R, lamw_dev, sizeof(double), sizeof(double), p1,
@@ -568,15 +612,6 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
   CK(cudaMemcpyAsync(lam_cur, lambda, sizeof(double) * R, cudaMemcpyHostToDevice, st));
   AL(D.beta[0], p1 * R);
   AL(D.beta[1], p1 * R);
-  AL(D.z, nR);
-  AL(D.theta, nR);
-  AL(D.rres, nR);
-  AL(D.s, nR);
-  AL(D.sdense, nR);
-  AL(D.Bq, (size_t)D.npad * D.ldk);
-  AL(D.Tsum, R);
-  AL(D.delta, R);
-  AL(D.sumth, R);
   for (int b = 0; b < 2; ++b) {
     // padded by 16 entries: the forward kernels copy metadata blocks in 16-byte units
     AL(D.sup_idx[b], X->p + 16);
@@ -584,26 +619,8 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
     AL(D.sup_c[b], (size_t)(X->p + 16) * R);
     AL(D.sup_b[b], (size_t)X->p * R);
   }
-  AL(D.sup_cnt, 2);
-  AL(D.cmax, 2 * R);
-  AL(D.sacc, nR);
-  AL(D.mterm, R);
-  AL(D.k1bar, 1);
-  AL(D.k2part, (size_t)std::max(ctx->k2_grid, ctx->sms * 8) * R * FSQR_NPART);
-  AL(D.ticket, 1);
-  AL(D.kbase, 1);
-  AL(D.fpart, (size_t)FIN_MAXGRID * R * FSQR_FPART);
-  AL(D.ftsum, (size_t)FIN_MAXGRID * R);
-  AL(D.fticket, 1 + FSQR_MAXR);
-  AL(D.scal, R * FSQR_NSCAL);
-  AL(D.status, R);
-  AL(D.commit_iter, R);
-  AL(D.iter, 1);
-  AL(D.stop, 1);
-  AL(D.lastR, R * FSQR_TRACE_W);
+  AL(D.tstamp, FSQR_TSTAMPS);
   AL(D.trace, (size_t)o.trace_cap * R * FSQR_TRACE_W);
-  AL(D.t_idx, R);
-  AL(D.pt_iters, R);
 
   // ---------------- a0: column statistics
   int* bad;
@@ -1080,6 +1097,14 @@ fsqr_status fsqr_set_tolerance(fsqr_ctx* ctx, double tol, int64_t max_iter) {
       ctx->graph[m].exec = nullptr;
     }
   }
+  return FSQR_OK;
+}
+
+fsqr_status fsqr_debug_stamps(fsqr_ctx* ctx, uint64_t* out_host, int64_t n) {
+  if (!ctx || !out_host || n < 0) return set_err(ctx, FSQR_ERR_CONFIG, "bad arguments");
+  SYNC_DEVICE();
+  CK(cudaMemcpy(out_host, ctx->D.tstamp, sizeof(uint64_t) * (size_t)std::min<int64_t>(n, FSQR_TSTAMPS),
+                cudaMemcpyDeviceToHost));
   return FSQR_OK;
 }
 

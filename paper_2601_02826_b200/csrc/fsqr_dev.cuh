@@ -24,6 +24,7 @@
 #define FSQR_FPART 8          // finalize partials per CTA and RHS: 7 sums + max|theta|
 #define FIN_THREADS 256
 #define FIN_MAXGRID 256       // ceil(65536 / FIN_THREADS)
+#define FSQR_TSTAMPS 2048     // per-CTA timing stamps of measurement builds
 #define FSQR_PATH_W 8         // path record: iters, Rp, Rb, Rz, obj, nnz, converged, loss sum
 
 // ST_SWITCH: path mode, w^k was just recorded as point t and becomes the start of point t+1
@@ -74,6 +75,7 @@ struct Dev {
   long long* sacc;                  // [R*n] int64 forward accumulators
   long long* mterm;                 // [R] the colsum term of the forward sums
   unsigned int* k1bar;              // [1] grid-barrier counter of k1_tcp's fused finalize
+  unsigned long long* tstamp;       // [FSQR_TSTAMPS] globaltimer stamps of instrumented builds (fsqr_debug_stamps)
   // K2 partials + last-CTA ticket
   double* k2part;                   // [grid][R][FSQR_NPART]
   unsigned int* ticket;
@@ -163,6 +165,12 @@ __device__ __forceinline__ int fwd_exponent(double cmax, long long cnt, int n) {
   frexp(cmax, &e2);
   return min(61 - e1, 43 - e2);
 }
+
+// release/acquire fence at GPU scope for the ticket pattern (writer: stores, fence, ticket atomic;
+// last CTA: ticket atomic, fence, loads).  __threadfence() is a sequentially consistent fence
+// (fence.sc.gpu), which measured up to 8 us on some SMs of the B200 in k1_tcp's tail; the
+// ticket pattern only needs acquire-release ordering.
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
@@ -397,6 +405,16 @@ __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, i
   const int gb = valid ? block_of_col(D, j) : 0;
   const double eta = valid ? D.eta[gb] : 1.0;
   const double inv_eta = valid ? D.inv_eta[gb] : 1.0;   // E14 multiplies by 1/eta_g
+  // every RHS's beta^k_j (and weight) is loaded before any store of this column: with several RHS
+  // the partial sums below write shared memory, which would otherwise keep the compiler from
+  // hoisting the next RHS's global load over them (one memory latency per RHS per column)
+  double bin[RMAX], win[RMAX];
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) {
+    const bool ld = valid && r < C.R;
+    bin[r] = ld ? C.beta_in[j * C.R + r] : 0.0;
+    win[r] = (ld && C.use_w) ? D.lamw[j * C.R + r] : 1.0;
+  }
   bool nz = false;
 #pragma unroll
   for (int r = 0; r < RMAX; ++r) {
@@ -406,8 +424,8 @@ __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, i
     double x[FSQR_NPART] = {0.0, 0.0, 0.0, 0.0, 0.0};
     double cm = 0.0;
     if (valid) {
-      const double b = C.beta_in[j * C.R + r];
-      const double lam = C.use_w ? C.cs->lam[r] * D.lamw[j * C.R + r] : C.cs->lam[r];
+      const double b = bin[r];
+      const double lam = C.use_w ? C.cs->lam[r] * win[r] : C.cs->lam[r];
       // KKT residual part of w^k and penalty at beta^k
       const double l2 = C.cs->lam2[r];
       const double d = b - soft_thr(b + (g[r] - l2 * b), lam);   // KKT: g - lam2 b in lam d|b|

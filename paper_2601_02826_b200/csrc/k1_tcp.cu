@@ -34,6 +34,11 @@
 //       iteration.  One launch instead of two.  (A first version let the last item of each row
 //       slab finalize that slab's 2048 rows: 8 records in one CTA put ~18 us on the tail.)
 #include <cuda.h>
+__device__ __forceinline__ unsigned __smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 
 #include "fin_common.cuh"
 
@@ -48,6 +53,9 @@
 #endif
 #ifndef K1P_CTAS
 #define K1P_CTAS 1     // CTAs per SM the launch grid assumes
+#endif
+#ifndef K1P_TIMING
+#define K1P_TIMING 0   // measurement build: per-CTA globaltimer stamps of iteration K1P_TIMING (fsqr_debug_stamps)
 #endif
 #ifndef K1P_DBG
 #define K1P_DBG 0   // measurement variants: bit 0 skips the MMAs, bit 1 the unpack, bit 2 the loads, bit 3 the atomics
@@ -129,6 +137,59 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
+
+// Fused finalize, record part (warps 4..11 of every CTA): records (r, b) of the active RHS in
+// contiguous shares per CTA, batches of <= NB records of one RHS.  The first batch's state rows and
+// constants are loaded BEFORE the grid barrier (every CTA's forward sums complete); after it only
+// the forward accumulators and the colsum term are on the critical path.  Called by all threads.
+template <int NB>
+__device__ __forceinline__ void fused_records(const Dev& D, long long kit, int R, int nblk, int q0, int q1, int t,
+                                              int wid, int tid, double* smd) {
+  FinRows<NB> pre;
+  FinRHS pc;
+  if (wid >= 4 && q0 < q1) {
+    const int r = q0 / nblk, b = q0 % nblk, nb = min(min(NB, nblk - b), q1 - q0);
+    if (D.status[r] == ST_ACTIVE) {
+      fin_load<NB>(D, r, b, nb, t, pre);
+      pc = fin_rhs(D, r, kit, 0);
+    }
+  }
+  // grid barrier: the grid is one CTA per SM and fully co-resident
+  fence_acq_rel_gpu();
+  __syncthreads();
+  if (tid == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(D.k1bar) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(D.k1bar) : "memory");
+    } while (v < gridDim.x);
+  }
+  __syncthreads();
+  if (wid < 4) return;
+#if K1P_TIMING
+  const long long rc0 = clock64();
+#endif
+  for (int q = q0; q < q1;) {
+    const int r = q / nblk, b = q % nblk, nb = min(min(NB, nblk - b), q1 - q);
+    if (D.status[r] == ST_ACTIVE) {
+      if (q == q0) {
+        pc.mt = __ldcg(D.mterm + r);
+        fin_records<NB>(D, r, b, nb, pc, t, 1, smd, pre);
+      } else {
+        FinRows<NB> w;
+        fin_load<NB>(D, r, b, nb, t, w);
+        const FinRHS c = fin_rhs(D, r, kit, __ldcg(D.mterm + r));
+        fin_records<NB>(D, r, b, nb, c, t, 1, smd, w);
+      }
+    }
+    q += nb;
+  }
+#if K1P_TIMING
+  grp_bar(1);
+  if (t == 0 && kit == K1P_TIMING) D.tstamp[8 * 148 + 200 + blockIdx.x] = (unsigned long long)(clock64() - rc0);
+#endif
+}
+
 template <int RMAX, int ST>
 __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, int cur) {
   using T = K1P<RMAX, ST>;
@@ -178,6 +239,10 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
   const uint32_t tmem_base = *tmem_slot;
   pdl_launch_dependents();
   pdl_wait();
+#if K1P_TIMING
+  unsigned long long ts0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts0));
+#endif
 
   const long long kit = *D.iter;
   const int par = (int)((kit + (cur ? 0 : 1)) & 1);
@@ -519,58 +584,72 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(T::TCOLS) : "memory");
   }
   if (!fused || stopped) return;
+#if K1P_TIMING
+  unsigned long long ts1, ts2, ts3, ts4;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts1));
+#endif
 
-  // ===================== fused finalize
-  // grid barrier: every CTA's forward sums (row atomics, colsum term) are complete and visible
-  __shared__ bool s_last;
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    atomicAdd(D.k1bar, 1u);
-    unsigned v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(D.k1bar) : "memory");
-    } while (v < gridDim.x);
-  }
-  __syncthreads();
-  // records (r, b) of the active RHS, contiguous shares per CTA, batches of <= 4 records of one RHS
-  // (warps 4..11 = one 256-thread group, named barrier 1; the A buffers are free scratch now)
+  // ===================== fused finalize (fused_records; the A buffers are free scratch now)
   double* smd = (double*)sA;
   long long* smll = (long long*)(smd + 4 * 8 * 9);
   const int nblk = (D.n + FG - 1) / FG;
-  if (wid >= 4) {
-    const int t = tid - 128;
-    const int tot = R * nblk, per = (tot + (int)gridDim.x - 1) / (int)gridDim.x;
-    const int q0 = min(tot, (int)blockIdx.x * per), q1 = min(tot, q0 + per);
-    for (int q = q0; q < q1;) {
-      const int r = q / nblk, b = q % nblk, nb = min(min(4, nblk - b), q1 - q);
-      if (D.status[r] == ST_ACTIVE) {
-        const FinRHS c = fin_rhs(D, r, kit, __ldcg(D.mterm + r));
-        fin_records<4>(D, r, b, nb, c, t, 1, smd);
-      }
-      q += nb;
-    }
-  }
+  const int tot = R * nblk, rper = (tot + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int q0 = min(tot, (int)blockIdx.x * rper), q1 = min(tot, q0 + rper);
+  const int t = tid - 128;
+  if (rper == 1) fused_records<1>(D, kit, R, nblk, q0, q1, t, wid, tid, smd);
+  else fused_records<4>(D, kit, R, nblk, q0, q1, t, wid, tid, smd);
   // ticket: the last CTA reduces every RHS's records in fixed order and ends the iteration
-  __threadfence();
+  __shared__ bool s_last;
+#if K1P_TIMING
+  ts2 = ts1;
+  unsigned long long ts2b, ts2c;
   __syncthreads();
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts2b));
+#endif
+  fence_acq_rel_gpu();
+  __syncthreads();
+#if K1P_TIMING
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts2c));
+#endif
   if (tid == 0) s_last = atomicAdd(D.fticket, 1u) == gridDim.x - 1;
   __syncthreads();
-  if (!s_last || wid < 4) return;
-  __threadfence();
-  const int t = tid - 128;
-  for (int r = 0; r < R; ++r) {
-    if (D.status[r] != ST_ACTIVE) continue;
-    const double b0v = D.beta[(int)(kit & 1)][r] + D.sumth[r] / D.eta[0];   // before fin_reduce_rhs rewrites sumth
-    grp_bar(1);
-    fin_reduce_rhs(D, r, nblk, b0v, kit, t, 1, smd, smll);
-    if (t == 0) D.mterm[r] = 0;
+#if K1P_TIMING
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts3));
+  if (tid == 0 && kit == K1P_TIMING) {
+    unsigned long long* st = D.tstamp + 8 * blockIdx.x;
+    st[0] = ts0; st[1] = ts1; st[2] = ts2; st[3] = ts2b; st[4] = ts2c; st[5] = ts3;
+    st[6] = (unsigned long long)__smid() | ((unsigned long long)s_last << 32);
+    st[7] = (unsigned long long)((nwork - blockIdx.x + gridDim.x - 1) / gridDim.x);
   }
+#endif
+  if (!s_last || wid < 4) return;
+  fence_acq_rel_gpu();
+#if K1P_TIMING
+  unsigned long long tq0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tq0));
+  if (t == 0 && kit == K1P_TIMING) D.tstamp[8 * 148 + 70] = tq0;
+#endif
+#if K1P_TIMING
+  long long cy0 = clock64();
+#endif
+  fin_reduce_all(D, nblk, kit, t, 1, smll);
+#if K1P_TIMING
+  {
+    long long dep = 0;
+    asm volatile("mov.u64 %0, 0;" : "=l"(dep) : "d"(D.delta[0]));
+    if (t == 0 && kit == K1P_TIMING) D.tstamp[8 * 148 + 74] = (unsigned long long)(clock64() + dep - cy0);
+  }
+#endif
+  if (t < R) D.mterm[t] = 0;
   fin_iteration_tail(D, kit, t);
   if (t == 0) {
     *D.fticket = 0u;
     *D.k1bar = 0u;   // every CTA has left the barrier (each took a ticket after it)
   }
+#if K1P_TIMING
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts4));
+  if (t == 0 && kit == K1P_TIMING) D.tstamp[8 * 148 + 40] = ts4;
+#endif
 }
 
 template <int RMAX, int ST>

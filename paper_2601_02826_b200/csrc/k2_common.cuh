@@ -6,6 +6,15 @@
 
 template <int RMAX>
 __device__ void k2_load_ctx(const Dev& D, K2Ctx<RMAX>& C) {
+  // clear the forward accumulators of the previous iteration (its finalize has completed: every
+  // K2 kernel calls this after griddepcontrol.wait; this iteration's forward product starts after
+  // this kernel ends).  Spread over the whole grid instead of a store per row on the finalize's
+  // critical path.
+  {
+    const size_t total = (size_t)D.R * D.n;
+    for (size_t o = (size_t)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += (size_t)gridDim.x * blockDim.x)
+      D.sacc[o] = 0;
+  }
   C.k = *D.iter;
   C.use_w = *D.use_w != 0;
   const int par = (int)(C.k & 1);
@@ -79,7 +88,7 @@ __device__ void k2_finish(const Dev& D, const K2Ctx<RMAX>& C, K2Part<RMAX>& P, d
     if (D.update && m > 0.0)
       atomicMax(D.cmax + (size_t)((C.k + 1) & 1) * D.R + r, (unsigned long long)__double_as_longlong(m));
   }
-  __threadfence();
+  fence_acq_rel_gpu();
   __syncthreads();
   if (tid == 0) {
     const unsigned t = atomicAdd(D.ticket, 1u);
@@ -87,7 +96,7 @@ __device__ void k2_finish(const Dev& D, const K2Ctx<RMAX>& C, K2Part<RMAX>& P, d
   }
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
+  fence_acq_rel_gpu();
 
   // ---------------- last CTA: R(w^k) for every active RHS (deterministic block sum over CTAs)
   __shared__ int s_rec[FSQR_MAXR];

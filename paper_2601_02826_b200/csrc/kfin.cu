@@ -228,14 +228,22 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize_mc(const Dev D) {
   const int nblk = gridDim.x;
   if (D.status[r] == ST_ACTIVE) {
     const FinRHS c = fin_rhs(D, r, k, D.mterm[r]);
-    fin_records<1>(D, r, blockIdx.x, 1, c, t, 0, smd);
-    __threadfence();
+    FinRows<1> w;
+    fin_load<1>(D, r, blockIdx.x, 1, t, w);
+    fin_records<1>(D, r, blockIdx.x, 1, c, t, 0, smd, w);
+    fence_acq_rel_gpu();
     __syncthreads();
     if (t == 0) s_last = atomicAdd(D.fticket + 1 + r, 1u) == (unsigned)nblk - 1;
     __syncthreads();
     if (s_last) {
-      __threadfence();
-      fin_reduce_rhs(D, r, nblk, c.b0, k, t, 0, smd, smll);
+      fence_acq_rel_gpu();
+      __shared__ int s_req;
+      if (t < 32) {
+        const bool req = fin_reduce_warp(D, r, nblk, c.b0, k, t);
+        if (t == 0) s_req = req ? 1 : 0;
+      }
+      __syncthreads();
+      if (s_req) fin_requant(D, r, t, 0, smll);
       if (t == 0) {
         D.mterm[r] = 0;
         D.fticket[1 + r] = 0u;
@@ -248,12 +256,12 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize_mc(const Dev D) {
     if (D.R == 1) return;
   }
   // ------------------------------------------------ last CTA overall: iteration tail
-  __threadfence();
+  fence_acq_rel_gpu();
   __syncthreads();
   if (t == 0) s_last = atomicAdd(D.fticket, 1u) == (unsigned)(nblk * D.R) - 1;
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
+  fence_acq_rel_gpu();
   fin_iteration_tail(D, k, t);
   if (t == 0) *D.fticket = 0u;
 }

@@ -181,3 +181,39 @@ def test_converged_state_passes_oracle_checks(cuda_ok, case):
         mb = np.linalg.norm(one["beta"] - b[r]) / (1 + np.linalg.norm(b[r]))
         mz = np.linalg.norm(one["z"] - z[r]) / (1 + np.linalg.norm(z[r]))
         assert max(mb, mz) <= tol, (case, tau, mb, mz)
+
+
+def test_c2_tuning_path_matches_oracle(cuda_ok):
+    """The paper's tuning protocol at C2 full size (Table 2's dimensions, tau = 0.5, G = 5): fsqr_tune
+    over the oracle reference's grid definition (T points, lambda_max -> lam_min_frac lambda_max,
+    reading R20) against the cached oracle path (tools/oracle_path_ref.py): identical update counts
+    and convergence flags at every point, identical supports, beta and objective per point, HBIC of
+    every point, and the same selected point."""
+    import paper_2601_02826_b200 as fs
+
+    fn = os.path.join(REF, "c2_path_tau0.5.npz")
+    if not os.path.exists(fn):
+        pytest.skip("tools/oracle_path_ref.py has not been run")
+    z = np.load(fn)
+    meta = json.loads(str(z["meta"]))
+    prob = datagen.make("c2")
+    assert design_checksum(prob) == meta["checksum"]
+    T, tau = meta["T"], meta["tau"]
+    X, y = to_device(prob)
+    S = fs.Solver(X, prob.storage, prob.n, prob.p, prob.ld, y, [tau], [1.0], G=meta["G"], mu=meta["mu"],
+                  eta=z["eta"], tol=meta["tol"], max_iter_point=meta["max_iter_point"])
+    out = S.tune(T=T, lam_min_frac=meta["lam_min_frac"])
+    np.testing.assert_allclose(out["grid"][0], z["grid"], rtol=1e-10)
+    res = S.path(out["grid"])          # the same path again, for the per-point records
+    np.testing.assert_array_equal(res["iters"][0], z["iters"])
+    np.testing.assert_array_equal(res["converged"][0], z["converged"])
+    np.testing.assert_allclose(res["obj"][0], z["obj"], rtol=1e-6)
+    np.testing.assert_allclose(out["hbic"][0], z["hbic"], rtol=1e-6)
+    assert int(out["best"][0]) == int(np.argmin(z["hbic"]))
+    off = np.concatenate([[0], np.cumsum(z["beta_cnt"])])
+    for t in range(T):
+        bo = np.zeros(prob.p + 1)
+        bo[z["beta_idx"][off[t]:off[t + 1]]] = z["beta_val"][off[t]:off[t + 1]]
+        bg = S.path_beta(0, t)
+        assert np.array_equal(bg != 0, bo != 0), t
+        assert rel(bg, bo) < 1e-6, t
