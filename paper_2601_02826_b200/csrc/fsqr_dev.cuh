@@ -375,15 +375,24 @@ struct K2Part {
   __device__ __forceinline__ void add(int r, const double (&x)[FSQR_NPART], double cm) {
     if constexpr (SM) {
       constexpr int W = FSQR_NPART + 1;
+      // the butterflies of the five sums and the max level by level (the same tree per value as
+      // warp_sum_d): the shuffles of one level are independent, so this is ~5 shuffle latencies per
+      // column and RHS instead of 30 back-to-back
+      double v[FSQR_NPART];
 #pragma unroll
-      for (int q = 0; q < FSQR_NPART; ++q) {
-        const double t = warp_sum_d(x[q]);
-        if ((threadIdx.x & 31) == 0) slot[r * W + q] += t;
-      }
+      for (int q = 0; q < FSQR_NPART; ++q) v[q] = x[q];
       double m = cm;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-      if ((threadIdx.x & 31) == 0) slot[r * W + FSQR_NPART] = fmax(slot[r * W + FSQR_NPART], m);
+      for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int q = 0; q < FSQR_NPART; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      }
+      if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int q = 0; q < FSQR_NPART; ++q) slot[r * W + q] += v[q];
+        slot[r * W + FSQR_NPART] = fmax(slot[r * W + FSQR_NPART], m);
+      }
     } else {
 #pragma unroll
       for (int q = 0; q < FSQR_NPART; ++q) v[r][q] += x[q];
@@ -405,16 +414,12 @@ __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, i
   const int gb = valid ? block_of_col(D, j) : 0;
   const double eta = valid ? D.eta[gb] : 1.0;
   const double inv_eta = valid ? D.inv_eta[gb] : 1.0;   // E14 multiplies by 1/eta_g
-  // every RHS's beta^k_j (and weight) is loaded before any store of this column: with several RHS
+  // every RHS's beta^k_j is loaded before any store of this column: with several RHS
   // the partial sums below write shared memory, which would otherwise keep the compiler from
   // hoisting the next RHS's global load over them (one memory latency per RHS per column)
-  double bin[RMAX], win[RMAX];
+  double bin[RMAX];
 #pragma unroll
-  for (int r = 0; r < RMAX; ++r) {
-    const bool ld = valid && r < C.R;
-    bin[r] = ld ? C.beta_in[j * C.R + r] : 0.0;
-    win[r] = (ld && C.use_w) ? D.lamw[j * C.R + r] : 1.0;
-  }
+  for (int r = 0; r < RMAX; ++r) bin[r] = (valid && r < C.R) ? C.beta_in[j * C.R + r] : 0.0;
   bool nz = false;
 #pragma unroll
   for (int r = 0; r < RMAX; ++r) {
@@ -425,7 +430,7 @@ __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, i
     double cm = 0.0;
     if (valid) {
       const double b = bin[r];
-      const double lam = C.use_w ? C.cs->lam[r] * win[r] : C.cs->lam[r];
+      const double lam = C.use_w ? C.cs->lam[r] * D.lamw[j * C.R + r] : C.cs->lam[r];
       // KKT residual part of w^k and penalty at beta^k
       const double l2 = C.cs->lam2[r];
       const double d = b - soft_thr(b + (g[r] - l2 * b), lam);   // KKT: g - lam2 b in lam d|b|
