@@ -108,9 +108,14 @@ typedef struct {
   int32_t power_max_iter;   /* power method cap (default 1000) */
   int32_t trace_cap;        /* rows of the per-iteration trace ring buffer (default 4096) */
   double power_tol;         /* power method relative tolerance (default 1e-4) */
-  uint64_t seed;            /* power-method start vector seed */
+  uint64_t seed;            /* power-method / Lanczos start vector seed */
   int64_t max_iter_point;   /* per-lambda-point cap in fsqr_path (default 10000) */
+  int32_t eta_method;       /* Lambda_hat_g by FSQR_ETA_LANCZOS (default) or FSQR_ETA_POWER (L259 names both);
+                               power_max_iter / power_tol are the step cap and relative tolerance of either */
+  int32_t pad_;
 } fsqr_options;
+
+enum { FSQR_ETA_LANCZOS = 0, FSQR_ETA_POWER = 1 };
 
 typedef struct {
   int64_t iterations;       /* outer iterations performed by this call */
@@ -125,7 +130,7 @@ typedef struct {
 typedef struct fsqr_ctx fsqr_ctx;
 
 /* Fills defaults: G=5, backend AUTO, mu=0 (=> 2/n, reading R2), eta_safety 1.05, tol 1e-6,
- * max_iter 100000, power 1000 / 1e-4, trace 4096, seed 0x5EED, max_iter_point 10000. */
+ * max_iter 100000, power 1000 / 1e-4, trace 4096, seed 0x5EED, max_iter_point 10000, eta by Lanczos. */
 void fsqr_default_options(fsqr_options* opt);
 
 /*
@@ -135,7 +140,8 @@ void fsqr_default_options(fsqr_options* opt);
  * l1 of E4, L150-155; copied and applied to every RHS; w_0 is ignored: the intercept is never
  * penalised), NULL = all ones.
  * Performs a0 (column statistics, exact integer sums for genotype storage),
- * a0' (eta_g by the power method unless opt->eta_host) and lambda_max (per tau);
+ * a0' (eta_g = eta_safety mu Lambda_hat_g by Lanczos or the power method, L259, unless
+ * opt->eta_host) and lambda_max (per tau);
  * cold start beta = 0, z = y, theta = 0.  Synchronises `stream`.
  */
 fsqr_status fsqr_create(const fsqr_design* X, const double* y_dev, int32_t n_rhs, const double* tau_host,

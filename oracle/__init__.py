@@ -14,6 +14,9 @@ Parity status per function (DESIGN.md §4 repeats this table):
   prox_beta/z     pinned: brute-force 1-D minimisation + SPEC worked values
   dual            pinned: SPEC worked values
   power           pinned: numpy.linalg.eigvalsh, identity and rank-one closed forms
+  lanczos         pinned: numpy.linalg.eigvalsh (to 1e-9 in a few steps), identity and rank-one (exact in
+                  one step), the tridiagonal bisection against eigvalsh of random tridiagonals, and
+                  Ritz value <= Lambda_max at every step count
   lambda_max      pinned: textbook null model (beta=0, intercept = sample quantile) just above it
   solve           pinned: LP vertex enumeration + HiGHS (tiny), Prop. 1 certificate, partition
                   invariance, fixed-point property, geometric decay (Corollary 1)
@@ -101,6 +104,10 @@ def _load():
         lib.orc_power_start.argtypes = [U64, I64]
         lib.orc_power.restype = D
         lib.orc_power.argtypes = [DP, I64, I64, D, I64, U64, P]
+        lib.orc_lanczos.restype = D
+        lib.orc_lanczos.argtypes = [DP, I64, I64, D, I64, U64, P]
+        lib.orc_tridiag_max_eig.restype = D
+        lib.orc_tridiag_max_eig.argtypes = [P, P, ctypes.c_int]
         lib.orc_lambda_max.restype = D
         lib.orc_lambda_max.argtypes = [DP, P, D, P]
         lib.orc_solve.restype = ctypes.c_int
@@ -230,11 +237,24 @@ def power(d: Design, j0: int, j1: int, tol: float = 1e-4, maxit: int = 1000, see
     return lam, int(it.value)
 
 
+def lanczos(d: Design, j0: int, j1: int, tol: float = 1e-4, maxit: int = 1000, seed: int = 0x5EED):
+    it = ctypes.c_int64(0)
+    lam = _load().orc_lanczos(d.ref, j0, j1, tol, maxit, seed, ctypes.byref(it))
+    return lam, int(it.value)
+
+
+def tridiag_max_eig(a, b) -> float:
+    a, b = _f64(a), _f64(b)
+    return _load().orc_tridiag_max_eig(_p(a), _p(b if len(b) else np.zeros(1)), len(a))
+
+
 def eta(d: Design, G: int, mu: float, safety: float = 1.05, tol: float = 1e-4, maxit: int = 1000,
-        seed: int = 0x5EED) -> np.ndarray:
-    """eta_g = safety * mu * Lambda_hat(X~_g^T X~_g) (L259; SURVEY §8(c) #1)."""
+        seed: int = 0x5EED, method: str = "power") -> np.ndarray:
+    """eta_g = safety * mu * Lambda_hat(X~_g^T X~_g) (L259), Lambda_hat by the power
+    method or by Lanczos (both named at L259)."""
     st = blocks(d.p + 1, G)
-    return np.array([safety * mu * power(d, int(st[g]), int(st[g + 1]), tol, maxit, seed)[0] for g in range(G)])
+    fn = power if method == "power" else lanczos
+    return np.array([safety * mu * fn(d, int(st[g]), int(st[g + 1]), tol, maxit, seed)[0] for g in range(G)])
 
 
 def lambda_max(d: Design, y, tau: float):

@@ -335,6 +335,92 @@ double orc_power(const orc_design* X, int64_t j0, int64_t j1, double tol, int64_
   return est;
 }
 
+/* Largest eigenvalue of the symmetric tridiagonal matrix with diagonal a[0..k-1] and off-diagonal
+ * b[0..k-2], by bisection on Sturm-sequence counts inside the Gershgorin bracket (textbook; 200
+ * halvings reach the fp64 resolution of any bracket). */
+static int sturm_below(const double* a, const double* b, int k, double x) {
+  int cnt = 0;
+  double q = a[0] - x;
+  if (q < 0.0) ++cnt;
+  for (int i = 1; i < k; ++i) {
+    if (q == 0.0) q = 1e-300;
+    q = (a[i] - x) - b[i - 1] * b[i - 1] / q;
+    if (q < 0.0) ++cnt;
+  }
+  return cnt;   /* number of eigenvalues < x */
+}
+
+double orc_tridiag_max_eig(const double* a, const double* b, int k) {
+  double lo = a[0], hi = a[0];
+  for (int i = 0; i < k; ++i) {
+    double r = (i > 0 ? fabs(b[i - 1]) : 0.0) + (i + 1 < k ? fabs(b[i]) : 0.0);
+    if (a[i] - r < lo) lo = a[i] - r;
+    if (a[i] + r > hi) hi = a[i] + r;
+  }
+  for (int it = 0; it < 200 && hi > lo; ++it) {
+    double mid = 0.5 * (lo + hi);
+    if (mid <= lo || mid >= hi) break;
+    if (sturm_below(a, b, k, mid) == k) hi = mid; else lo = mid;
+  }
+  return hi;
+}
+
+/* Lambda_max(X~_g^T X~_g) for model columns [j0, j1) by the Lanczos method (L259: "the power method
+ * ... or Lanczos"), from the same seeded start vector as orc_power:
+ *   v_1 = start/||start||, beta_0 = 0;  for k = 1, 2, ...:
+ *     w = X~_g^T (X~_g v_k);  alpha_k = v_k^T w;  w -= alpha_k v_k + beta_{k-1} v_{k-1};  beta_k = ||w||
+ *     est_k = largest eigenvalue of tridiag(alpha_1..k; beta_1..k-1)  (Ritz value, <= Lambda_max)
+ *     stop when |est_k - est_{k-1}| <= tol * est_k, beta_k = 0 (invariant subspace: exact), or k = maxit
+ *     v_{k+1} = w / beta_k
+ * (no reorthogonalisation: the largest Ritz value converges regardless). */
+double orc_lanczos(const orc_design* X, int64_t j0, int64_t j1, double tol, int64_t maxit, uint64_t seed,
+                   int64_t* iters) {
+  int64_t m = j1 - j0, n = X->n;
+  double* v = (double*)malloc(sizeof(double) * m);
+  double* vp = (double*)calloc((size_t)m, sizeof(double));
+  double* w = (double*)malloc(sizeof(double) * m);
+  double* u = (double*)malloc(sizeof(double) * n);
+  double* al = (double*)malloc(sizeof(double) * (maxit + 1));
+  double* be = (double*)malloc(sizeof(double) * (maxit + 1));
+  double nv = 0.0;
+  for (int64_t a = 0; a < m; ++a) { v[a] = orc_power_start(seed, j0 + a); nv += v[a] * v[a]; }
+  nv = sqrt(nv);
+  for (int64_t a = 0; a < m; ++a) v[a] /= nv;
+  double est = 0.0, prev = 0.0, bprev = 0.0;
+  int64_t k;
+  for (k = 1; k <= maxit; ++k) {
+    orc_fwdprod_range(X, v, j0, j1, u);
+    orc_backprod_range(X, u, j0, j1, w);
+    double alpha = 0.0;
+    for (int64_t a = 0; a < m; ++a) alpha += v[a] * w[a];
+    double nw = 0.0;
+    for (int64_t a = 0; a < m; ++a) {
+      w[a] = w[a] - alpha * v[a] - bprev * vp[a];
+      nw += w[a] * w[a];
+    }
+    double beta = sqrt(nw);
+    al[k - 1] = alpha;
+    est = orc_tridiag_max_eig(al, be, (int)k);
+    if (k > 1 && fabs(est - prev) <= tol * est) break;
+    if (!(beta > 1e-12 * fabs(alpha))) break;
+    prev = est;
+    be[k - 1] = beta;
+    for (int64_t a = 0; a < m; ++a) {
+      vp[a] = v[a];
+      v[a] = w[a] / beta;
+    }
+    bprev = beta;
+  }
+  if (iters) *iters = k > maxit ? maxit : k;
+  free(v);
+  free(vp);
+  free(w);
+  free(u);
+  free(al);
+  free(be);
+  return est;
+}
+
 /* ----------------------------------------------------------- lambda_max */
 
 static int cmp_double(const void* a, const void* b) {

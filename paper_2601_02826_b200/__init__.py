@@ -24,6 +24,7 @@ _lib = None
 F32_DENSE, U8, PACKED2 = 0, 1, 2
 SCAD, MCP = 1, 2
 BACKEND_AUTO, BACKEND_TC, BACKEND_SIMT = 0, 1, 2
+ETA_LANCZOS, ETA_POWER = 0, 1
 STATUS = {0: "FSQR_OK", 2: "FSQR_NOT_CONVERGED", -1: "FSQR_ERR_CONFIG", -2: "FSQR_ERR_DATA",
           -3: "FSQR_ERR_NUMERIC", -4: "FSQR_ERR_CUDA", -5: "FSQR_ERR_OOM", -6: "FSQR_ERR_STATE"}
 
@@ -47,7 +48,8 @@ class fsqr_options(ctypes.Structure):
     _fields_ = [("G", ctypes.c_int32), ("backend", ctypes.c_int32), ("mu", ctypes.c_double),
                 ("eta_safety", ctypes.c_double), ("eta_host", ctypes.c_void_p), ("tol", ctypes.c_double),
                 ("max_iter", ctypes.c_int64), ("power_max_iter", ctypes.c_int32), ("trace_cap", ctypes.c_int32),
-                ("power_tol", ctypes.c_double), ("seed", ctypes.c_uint64), ("max_iter_point", ctypes.c_int64)]
+                ("power_tol", ctypes.c_double), ("seed", ctypes.c_uint64), ("max_iter_point", ctypes.c_int64),
+                ("eta_method", ctypes.c_int32), ("pad_", ctypes.c_int32)]
 
 
 class fsqr_tune_options(ctypes.Structure):

@@ -253,8 +253,8 @@ __device__ __forceinline__ void fin_records(const Dev& D, int r, int b0, int nb,
 // All nblk records of RHS r are written: ONE WARP reduces them in record order (lane l adds records
 // l, l + 32, ..., all nine values of a record in one round of loads; then a level-major butterfly),
 // and lane 0 publishes R_p, R_z, the loss and sum theta^{k+1}, beta_0^{k+1} and delta^{k+1}.
-// Returns (on every lane) whether max|theta^{k+1}| left the binade of delta^k: then every row must
-// be re-quantised with delta^{k+1} = 2^(e-28) (fin_requant).  Several RHS reduce on different warps.
+// Returns (on every lane) whether max|theta^{k+1}| / delta^k left [2^26, 2^28): then every row must be
+// re-quantised with delta^{k+1} = 2^(e-28) (fin_requant).  Several RHS reduce on different warps.
 __device__ __forceinline__ bool fin_reduce_warp(const Dev& D, int r, int nblk, double b0, long long k, int lane) {
   double a[7] = {0, 0, 0, 0, 0, 0, 0};
   double mx = 0.0;
@@ -279,12 +279,17 @@ __device__ __forceinline__ bool fin_reduce_warp(const Dev& D, int r, int nblk, d
     mx = (m > mx || !isfinite(m)) ? m : mx;
     tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
   }
+  // The scale delta^k is kept while max|theta^{k+1}| / delta^k stays in [2^26, 2^28): every T then
+  // has 26..28 significant bits and |T| < 2^28 (the int64 bounds of K2's reconstruction).  Leaving
+  // that range (one binade of hysteresis downwards, none upwards) re-quantises every row with
+  // delta^{k+1} = 2^(e - 28), e the binary exponent of max|theta^{k+1}|.
   const int e_new = theta_exponent(mx);
   const int e_old = theta_exponent(dprev * ldexp(1.0, 28) * 0.75);   // delta^k = 2^(e_old - 28)
-  const bool requant = e_new != e_old;
+  const bool live = mx > 0.0 && isfinite(mx);
+  const bool requant = !live || e_new > e_old || e_new < e_old - 1;
   const double rp = sqrt(a[0]) / (1.0 + sqrt(a[6]));
   const double rz = sqrt(a[3]) / (1.0 + sqrt(a[1]) + sqrt(a[2]));
-  const double dnew = (mx > 0.0 && isfinite(mx)) ? ldexp(1.0, e_new - 28) : 1.0;
+  const double dnew = !requant ? dprev : (live ? ldexp(1.0, e_new - 28) : 1.0);
   if (lane == 0) {
     double* sc = D.scal + r * FSQR_NSCAL;
     sc[0] = rp;

@@ -33,6 +33,10 @@ void launch_power_reduce(const Dev& D, const int64_t* bstart, const double* v, c
                          double* est, double* nrm, cudaStream_t st);
 void launch_power_norm(const Dev& D, double* v, const double* w, const double* nrm, const int* frozen,
                        cudaStream_t st);
+void launch_lanczos_orth(const Dev& D, const double* v, const double* vp, double* w, const double* alpha,
+                         const double* beta, const int* frozen, cudaStream_t st);
+void launch_lanczos_next(const Dev& D, double* v, double* vp, const double* w, const double* beta, const int* frozen,
+                         cudaStream_t st);
 void launch_null_score(const double* y, int n, const double* tau, int R, double* psi, cudaStream_t st);
 void launch_power_fwd_int(const Dev& D, const int64_t* bstart, const double* v, const int* frozen, double* part,
                           int S, double* u, double* Ug, cudaStream_t st);
@@ -250,6 +254,35 @@ fsqr_status init_state(fsqr_ctx* ctx, cudaStream_t st) {
   return FSQR_OK;
 }
 
+// largest eigenvalue of the symmetric tridiagonal Lanczos matrix (diagonal a, off-diagonal b,
+// b.size() == a.size() - 1): bisection on Sturm counts inside the Gershgorin interval
+double tridiag_top(const std::vector<double>& a, const std::vector<double>& b) {
+  const int k = (int)a.size();
+  double lo = a[0], hi = a[0];
+  for (int i = 0; i < k; ++i) {
+    const double rad = (i > 0 ? std::fabs(b[i - 1]) : 0.0) + (i + 1 < k ? std::fabs(b[i]) : 0.0);
+    lo = std::min(lo, a[i] - rad);
+    hi = std::max(hi, a[i] + rad);
+  }
+  auto below = [&](double x) {   // eigenvalues < x
+    int cnt = 0;
+    double q = a[0] - x;
+    cnt += q < 0.0;
+    for (int i = 1; i < k; ++i) {
+      if (q == 0.0) q = 1e-300;
+      q = (a[i] - x) - b[i - 1] * b[i - 1] / q;
+      cnt += q < 0.0;
+    }
+    return cnt;
+  };
+  for (int it = 0; it < 200 && hi > lo; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (mid <= lo || mid >= hi) break;
+    if (below(mid) == k) hi = mid; else lo = mid;
+  }
+  return hi;
+}
+
 fsqr_status power_method(fsqr_ctx* ctx, cudaStream_t st) {
   Dev& D = ctx->D;
   const int G = D.G;
@@ -283,6 +316,52 @@ fsqr_status power_method(fsqr_ctx* ctx, cudaStream_t st) {
   std::vector<double> h_est(G), prev(G, 0.0), lam(G, 0.0), h_nrm(G);
   std::vector<int> frozen(G, 0);
   int live = G;
+  if (ctx->opt.eta_method == FSQR_ETA_LANCZOS) {
+    // Lanczos (L259): alpha_k = v^T X~_g^T X~_g v, w -= alpha v + beta_{k-1} v_{k-1}, beta_k = ||w||;
+    // the estimate is the largest eigenvalue of the tridiagonal T_k (Ritz value <= Lambda_max)
+    double *vp, *alpha, *beta, *junk;
+    AL(vp, p1);
+    AL(alpha, G);
+    AL(beta, G);
+    AL(junk, G);
+    std::vector<std::vector<double>> ta(G), tb(G);
+    std::vector<double> h_alpha(G), h_beta(G);
+    for (int it = 1; it <= ctx->opt.power_max_iter && live > 0; ++it) {
+      if (geno) {
+        launch_power_fwd_int(D, d_bs, v, d_frozen, part, S, u, Ug, st);
+        launch_back_int(D, u, Ug, 1, d_frozen, w, nullptr, st);
+      } else {
+        launch_power_fwd(D, d_bs, v, d_frozen, u, st);
+        launch_back_f64(D, u, 1, d_frozen, w, nullptr, st);
+      }
+      launch_power_reduce(D, d_bs, v, w, d_frozen, alpha, junk, st);
+      launch_lanczos_orth(D, v, vp, w, alpha, beta, d_frozen, st);
+      launch_power_reduce(D, d_bs, w, w, d_frozen, junk, beta, st);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(h_alpha.data(), alpha, sizeof(double) * G, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h_beta.data(), beta, sizeof(double) * G, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int g = 0; g < G; ++g) {
+        if (frozen[g]) continue;
+        ta[g].push_back(h_alpha[g]);
+        lam[g] = tridiag_top(ta[g], tb[g]);
+        if ((it > 1 && std::fabs(lam[g] - prev[g]) <= ctx->opt.power_tol * lam[g]) ||
+            !(h_beta[g] > 1e-12 * std::fabs(h_alpha[g]))) {
+          frozen[g] = 1;
+          --live;
+        } else {
+          tb[g].push_back(h_beta[g]);
+        }
+        prev[g] = lam[g];
+      }
+      CK(cudaMemcpyAsync(d_frozen, frozen.data(), sizeof(int) * G, cudaMemcpyHostToDevice, st));
+      launch_lanczos_next(D, v, vp, w, beta, d_frozen, st);
+    }
+    CK(cudaStreamSynchronize(st));
+    ctx->eta.resize(G);
+    for (int g = 0; g < G; ++g) ctx->eta[g] = ctx->opt.eta_safety * ctx->opt.mu * lam[g];
+    return FSQR_OK;
+  }
   for (int it = 1; it <= ctx->opt.power_max_iter && live > 0; ++it) {
     if (geno) {
       launch_power_fwd_int(D, d_bs, v, d_frozen, part, S, u, Ug, st);
@@ -365,6 +444,7 @@ void fsqr_default_options(fsqr_options* o) {
   o->power_tol = 1e-4;
   o->seed = 0x5EED;
   o->max_iter_point = 10000;
+  o->eta_method = FSQR_ETA_LANCZOS;
 }
 
 const char* fsqr_status_str(fsqr_status s) {
@@ -446,6 +526,8 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
   if (o.G < 1 || (int64_t)o.G > X->p + 1) return set_err(ctx, FSQR_ERR_CONFIG, "G=%d not in [1, p+1]", o.G);
   if (!(o.eta_safety > 1.0) && !o.eta_host) return set_err(ctx, FSQR_ERR_CONFIG, "eta_safety must be > 1");
   if (o.max_iter < 0 || o.power_max_iter < 1 || o.trace_cap < 1) return set_err(ctx, FSQR_ERR_CONFIG, "bad iteration caps");
+  if (o.eta_method != FSQR_ETA_LANCZOS && o.eta_method != FSQR_ETA_POWER)
+    return set_err(ctx, FSQR_ERR_CONFIG, "eta_method %d unknown", o.eta_method);
   for (int r = 0; r < R; ++r) {
     if (!(tau[r] > 0.0 && tau[r] < 1.0)) return set_err(ctx, FSQR_ERR_CONFIG, "tau[%d]=%g not in (0,1)", r, tau[r]);
     if (!(lambda[r] >= 0.0) || !std::isfinite(lambda[r])) return set_err(ctx, FSQR_ERR_CONFIG, "lambda[%d]=%g invalid", r, lambda[r]);

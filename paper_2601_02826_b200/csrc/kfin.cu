@@ -569,6 +569,28 @@ __global__ void k_power_norm(const Dev D, double* v, const double* w, const doub
   }
 }
 
+// Lanczos step (a0', L259): w_g <- w_g - alpha_g v_g - beta_g vp_g for the live blocks (alpha, beta
+// device arrays [G]; beta_g of the previous step, 0 at the first)
+__global__ void k_lanczos_orth(const Dev D, const double* v, const double* vp, double* w, const double* alpha,
+                               const double* beta, const int* frozen) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= D.p; j += (int64_t)gridDim.x * blockDim.x) {
+    const int g = block_of_col(D, j);
+    if (frozen[g]) continue;
+    w[j] = w[j] - alpha[g] * v[j] - beta[g] * vp[j];
+  }
+}
+
+// vp_g <- v_g, v_g <- w_g / beta_g for the live blocks
+__global__ void k_lanczos_next(const Dev D, double* v, double* vp, const double* w, const double* beta,
+                               const int* frozen) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= D.p; j += (int64_t)gridDim.x * blockDim.x) {
+    const int g = block_of_col(D, j);
+    if (frozen[g]) continue;
+    vp[j] = v[j];
+    v[j] = w[j] / beta[g];
+  }
+}
+
 // sample tau-quantile by exact rank selection and the null-model score psi/n (DESIGN reading R4)
 __global__ void k_null_score(const double* y, int n, const double* tau, int R, double* psi /*[R][n]*/) {
   __shared__ double ys[2048];
@@ -789,6 +811,14 @@ void launch_power_reduce(const Dev& D, const int64_t* bstart, const double* v, c
 void launch_power_norm(const Dev& D, double* v, const double* w, const double* nrm, const int* frozen,
                        cudaStream_t st) {
   k_power_norm<<<512, 256, 0, st>>>(D, v, w, nrm, frozen);
+}
+void launch_lanczos_orth(const Dev& D, const double* v, const double* vp, double* w, const double* alpha,
+                         const double* beta, const int* frozen, cudaStream_t st) {
+  k_lanczos_orth<<<512, 256, 0, st>>>(D, v, vp, w, alpha, beta, frozen);
+}
+void launch_lanczos_next(const Dev& D, double* v, double* vp, const double* w, const double* beta, const int* frozen,
+                         cudaStream_t st) {
+  k_lanczos_next<<<512, 256, 0, st>>>(D, v, vp, w, beta, frozen);
 }
 void launch_power_fwd_int(const Dev& D, const int64_t* bstart, const double* v, const int* frozen, double* part,
                           int S, double* u, double* Ug, cudaStream_t st) {

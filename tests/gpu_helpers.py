@@ -15,7 +15,7 @@ def to_device(prob):
 
 
 def make_pair(name, n=None, p=None, seed=None, storage=None, G=None, taus=None, lam_frac=None, mu=None,
-              backend=0, oracle_eta=True, tol=1e-6, max_iter=100000):
+              backend=0, oracle_eta=True, tol=1e-6, max_iter=100000, **kw):
     """Return (prob, oracle Design, solver, dict of shared settings).  eta comes from the ORACLE
     (power method on the CPU) and is handed to the GPU, never the other way round."""
     import paper_2601_02826_b200 as fs
@@ -31,7 +31,7 @@ def make_pair(name, n=None, p=None, seed=None, storage=None, G=None, taus=None, 
     eta = oracle.eta(d, G, mu) if oracle_eta else None
     X, y = to_device(prob)
     S = fs.Solver(X, prob.storage, prob.n, prob.p, prob.ld, y, taus, lams, G=G, mu=mu, tol=tol, max_iter=max_iter,
-                  backend=backend, eta=eta)
+                  backend=backend, eta=eta, **kw)
     return prob, d, S, dict(taus=taus, lams=lams, G=G, mu=mu, eta=eta, lm=lm)
 
 

@@ -21,15 +21,20 @@ def _oracle_run(prob, d, cfg, r, k):
     return oracle.solve(d, prob.y, cfg["taus"][r], lamv, cfg["eta"], cfg["mu"], cfg["G"], max_iter=k, check=False)
 
 
-def test_colstats_lambda_max_eta(cuda_ok):
+@pytest.mark.parametrize("name,storage", [("c2", 1), ("c4", 2), ("c1", 0)])
+@pytest.mark.parametrize("method", ["lanczos", "power"])
+def test_colstats_lambda_max_eta(cuda_ok, name, storage, method):
+    """a0 column statistics, lambda_max (reading R4) and eta_g (L259) by Lanczos (the default) or the
+    power method, each against the oracle's same method from the same seeded start vector."""
     import paper_2601_02826_b200 as fs
 
-    prob, d, S, cfg = make_pair("c2", n=700, p=1500, oracle_eta=False)
+    prob, d, S, cfg = make_pair(name, n=700, p=1500, storage=storage, oracle_eta=False,
+                                eta_method=fs.ETA_LANCZOS if method == "lanczos" else fs.ETA_POWER)
     m, s = S.colstats()
     np.testing.assert_allclose(m, d.mean, rtol=1e-13)
     np.testing.assert_allclose(s, d.sd, rtol=1e-12)
     np.testing.assert_allclose(S.lambda_max(), cfg["lm"], rtol=1e-10)
-    eta_orc = oracle.eta(d, cfg["G"], cfg["mu"])
+    eta_orc = oracle.eta(d, cfg["G"], cfg["mu"], method=method)
     np.testing.assert_allclose(S.eta(), eta_orc, rtol=1e-6)
 
 

@@ -181,6 +181,56 @@ def test_power_closed_forms():
     assert est == pytest.approx(np.dot(uu, uu) * np.dot(v, v), rel=1e-6)
 
 
+def test_tridiag_max_eig_vs_eigvalsh():
+    rng = np.random.default_rng(5)
+    for k in (1, 2, 3, 7, 20, 60):
+        a = rng.normal(size=k) * 3
+        b = rng.normal(size=k - 1)
+        T = np.diag(a) + np.diag(b, 1) + np.diag(b, -1)
+        assert oracle.tridiag_max_eig(a, b) == pytest.approx(np.linalg.eigvalsh(T)[-1], rel=1e-13, abs=1e-13)
+
+
+def test_lanczos_vs_eigvalsh_and_power():
+    """Lanczos (L259) reaches the largest eigenvalue of X~_g^T X~_g far sooner than the power method;
+    its Ritz value never exceeds Lambda_max (interlacing)."""
+    for seed, (n, p) in enumerate([(60, 9), (200, 50), (40, 39), (120, 7), (300, 240)]):
+        prob = datagen.make("c2", n=n, p=p, seed=100 + seed)
+        d = oracle.Design.from_problem(prob)
+        A, _, _ = _np_standardized(prob)
+        st = oracle.blocks(p + 1, 3)
+        for g in range(3):
+            B = A[:, st[g]:st[g + 1]]
+            ref = np.linalg.eigvalsh(B.T @ B)[-1]
+            est, it = oracle.lanczos(d, int(st[g]), int(st[g + 1]), tol=1e-12, maxit=1000)
+            assert est == pytest.approx(ref, rel=1e-9)
+            for k in (1, 2, 3):
+                e_k, _ = oracle.lanczos(d, int(st[g]), int(st[g + 1]), tol=0.0, maxit=k)
+                assert e_k <= ref * (1 + 1e-12)
+            e4, it4 = oracle.lanczos(d, int(st[g]), int(st[g + 1]), tol=1e-4, maxit=1000)
+            p4, ip4 = oracle.power(d, int(st[g]), int(st[g + 1]), tol=1e-4, maxit=1000)
+            assert abs(e4 - ref) <= 1e-3 * ref
+            assert it4 <= ip4
+
+
+def test_lanczos_closed_forms():
+    """identity block -> 1 after one step (beta_1 = 0); rank-one block -> ||u||^2 ||v||^2 after at most two
+    (the Krylov space of a rank-one matrix has dimension 2)."""
+    n, p = 8, 5
+    X = np.zeros((p, 8), dtype=np.float32)
+    for c in range(p):
+        X[c, c] = 1.0
+    d = oracle.Design(0, n, p, 8, X, mean=np.zeros(p), sd=np.ones(p))
+    est, it = oracle.lanczos(d, 1, p + 1, tol=1e-14, maxit=1000)
+    assert est == pytest.approx(1.0, rel=1e-12) and it == 1
+    u = np.array([1, 2, 0, -1, 3, 0, 1, 1], dtype=np.float64)
+    v = np.array([0.5, -1, 2, 1, 0.25])
+    X = np.outer(v, u).astype(np.float32)
+    d = oracle.Design(0, n, p, 8, X, mean=np.zeros(p), sd=np.ones(p))
+    est, it = oracle.lanczos(d, 1, p + 1, tol=1e-14, maxit=1000)
+    uu = X[0].astype(np.float64) / v[0]
+    assert est == pytest.approx(np.dot(uu, uu) * np.dot(v, v), rel=1e-12) and it <= 2
+
+
 # ----------------------------------------------------------------- solver pins
 
 def _tiny(seed, n=12, p=3, tau=0.5):

@@ -5,9 +5,9 @@ TEST/MEASUREMENT INFRASTRUCTURE: runs only oracle/ (plain fp64 C, OpenMP over al
 fixed-order sums) on the seeded datagen/ inputs; nothing from the CUDA path.  For each config:
 
   * s/iter: median over K timed oracle iterations of Algorithm 1 (one X~^T theta pass over every
-    column + the support forward product), after a short untimed warm-up so the support is
-    non-trivial; the step sizes come from a cheap valid eta (the trace bound
-    1.05 mu sum_j ||x~_j||^2 >= 1.05 mu Lambda_max, which does not change the per-iteration cost);
+    column + the support forward product), after a short untimed warm-up from the cold start at the
+    config's lambda, with the oracle's own eta (the committed full-size references' where they
+    exist, else Lanczos), so the support, hence the forward product's cost, is the real one;
   * optionally the same with OMP_NUM_THREADS=1 (C1, C2);
   * optionally time to R <= tol from the cold start with the oracle's own power-method eta
     (C1 at 1e-6, C2 tau=0.5 at 1e-4), wall seconds and iterations.
@@ -41,6 +41,16 @@ def emit(d, out):
             f.write(line + "\n")
 
 
+def ref_eta(name: str):
+    """the oracle's own eta from the committed full-size references (tools/oracle_ref.py), if any"""
+    key = "m" if name in ("m", "c5") else name
+    ref = os.path.join(ROOT, "tests", "golden", "oracle_ref")
+    for fn in sorted(os.listdir(ref)) if os.path.isdir(ref) else []:
+        if fn.startswith(("m_", "c5_") if key == "m" else (key + "_tau",)):
+            return np.load(os.path.join(ref, fn))["eta"]
+    return None
+
+
 def s_per_iter(name: str, iters: int, warm: int):
     prob = datagen.make(name)
     d = oracle.Design.from_problem(prob)
@@ -49,9 +59,9 @@ def s_per_iter(name: str, iters: int, warm: int):
     frac = prob.lam_frac if prob.path_points == 1 else 0.1
     lm, _ = oracle.lambda_max(d, prob.y, tau)
     lam = oracle.lam_vector(prob.p, frac * lm)
-    # trace bound per block: sum_j ||x~_j||^2 = (n - 1) per standardised column, n for the intercept
-    st = oracle.blocks(prob.p + 1, G)
-    eta = 1.05 * mu * (prob.n - 1) * np.diff(st).astype(np.float64)
+    eta = ref_eta(name)
+    if eta is None:
+        eta = oracle.eta(d, G, mu, method="lanczos")
     w = oracle.solve(d, prob.y, tau, lam, eta, mu, G, max_iter=warm, check=False)
     state = (w["beta"], w["z"], w["theta"])
     ts = []

@@ -5,7 +5,8 @@ TEST INFRASTRUCTURE: this script calls only ``oracle/`` (the fp64 CPU FS-QRPPA) 
 (the seeded inputs); nothing here comes from the CUDA path.  For each BASELINE.json config at its
 full size it runs, from the cold start (beta = 0, z = y, theta = 0; reading R5):
 
-  * the oracle's own power method for eta_g = 1.05 mu Lambda_max(X~_g^T X~_g) (L259, reading R3),
+  * the oracle's own power method (or Lanczos, --eta-method) for eta_g = 1.05 mu Lambda_max(X~_g^T X~_g)
+    (L259, reading R3),
   * lambda = frac * lambda_max(tau) (reading R4; frac from the config, C5 at a mid-path point),
   * exactly K = 200 iterations of Algorithm 1 (``oracle.solve(check=False)``),
   * R(w^K) (reading R1) and the objective E1 at beta^K,
@@ -72,7 +73,7 @@ def cached_eta(name: str, cks: str):
     return None
 
 
-def run(name: str, iters: int, prob=None, d=None, eta=None, log=print):
+def run(name: str, iters: int, prob=None, d=None, eta=None, log=print, eta_method: str = "power"):
     t0 = time.perf_counter()
     if prob is None:
         prob = datagen.make(name)
@@ -85,7 +86,7 @@ def run(name: str, iters: int, prob=None, d=None, eta=None, log=print):
         eta = cached_eta(name, cks)
     if eta is None:
         t0 = time.perf_counter()
-        eta = oracle.eta(d, G, mu)
+        eta = oracle.eta(d, G, mu, method=eta_method)
         t_eta = time.perf_counter() - t0
     log(f"{name}: datagen {t_gen:.1f} s, eta {t_eta:.1f} s")
     taus = C5_TAUS if name == "c5" else prob.taus
@@ -102,7 +103,7 @@ def run(name: str, iters: int, prob=None, d=None, eta=None, log=print):
         obj = oracle.objective(d, prob.y, tau, lv, o["beta"])
         nz = np.flatnonzero(o["beta"])
         fn = os.path.join(OUT, f"{name}_tau{tau:.1f}.npz")
-        meta = dict(config=name, tau=tau, n=prob.n, p=prob.p, G=G, mu=mu, lam_frac=frac, iters=iters,
+        meta = dict(config=name, tau=tau, n=prob.n, p=prob.p, G=G, mu=mu, lam_frac=frac, iters=iters, eta_method=eta_method,
                     checksum=cks, oracle_s_per_iter=t_solve / iters, threads=os.cpu_count(),
                     script="tools/oracle_ref.py (oracle/ + datagen/ only)")
         np.savez_compressed(fn, eta=eta, lam=lam, lambda_max=lm, q=q, beta_idx=nz.astype(np.int64),
@@ -116,6 +117,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="m,c5,c3,c4")
     ap.add_argument("--iters", type=int, default=200)
+    ap.add_argument("--eta-method", dest="eta_method", default="power", choices=["power", "lanczos"])
     a = ap.parse_args()
     names = a.configs.split(",")
     cache = {}
@@ -123,7 +125,7 @@ def main():
         # M and C5 share the design, the response and G, hence eta
         key = "m" if name in ("m", "c5") else name
         prob, d, eta = cache.get(key, (None, None, None))
-        prob, d, eta = run(name, a.iters, prob, d, eta, log=lambda s: print(s, flush=True))
+        prob, d, eta = run(name, a.iters, prob, d, eta, log=lambda s: print(s, flush=True), eta_method=a.eta_method)
         cache = {key: (prob, d, eta)}
 
 
