@@ -39,6 +39,11 @@
 #ifndef K2TC2_CW
 #define K2TC2_CW 8   // converter warps (two per SM sub-partition: the unpack loop is latency-bound with one)
 #endif
+#ifndef K2TC2_CWM
+#define K2TC2_CWM 4  // converter warps with several RHS (8 would need a 640-thread block: 96 registers and
+                     // spills; setmaxnreg per warpgroup did not help -- ptxas keeps the launch bound)
+#endif
+
 
 namespace {
 
@@ -56,7 +61,7 @@ struct Cfg2 {
   // up to 4 RHS: 8 converter warps, 4 epilogue warps; more: the per-column epilogue (E14, KKT
   // partials and support entries for every RHS) is the slower side, so 4 converters and two sets
   // of 4 epilogue warps taking alternate tiles (one accumulator buffer each)
-  static constexpr int CW = NPAD == 16 ? K2TC2_CW : 4;   // (4 converters at NPAD = 16 would spill)
+  static constexpr int CW = NPAD == 16 ? K2TC2_CW : K2TC2_CWM;   // (4 converters at NPAD = 16 would spill)
   static constexpr int EW = NPAD == 16 ? 4 : 8;
   // NPAD == 16: one accumulator per code plane q, so the converter can leave the codes in place
   // ((w & (3 << 2q)) = x * 4^q, one LOP per word instead of shift + mask); the epilogue divides
