@@ -255,20 +255,33 @@ __device__ __forceinline__ void fin_records(const Dev& D, int r, int b0, int nb,
 // and lane 0 publishes R_p, R_z, the loss and sum theta^{k+1}, beta_0^{k+1} and delta^{k+1}.
 // Returns (on every lane) whether max|theta^{k+1}| / delta^k left [2^26, 2^28): then every row must be
 // re-quantised with delta^{k+1} = 2^(e-28) (fin_requant).  Several RHS reduce on different warps.
-__device__ __forceinline__ bool fin_reduce_warp(const Dev& D, int r, int nblk, double b0, long long k, int lane) {
+__device__ __forceinline__ bool fin_reduce_warp(const Dev& D, int r, int nblk, double b0, long long k, int lane,
+                                                bool commit = true) {
   double a[7] = {0, 0, 0, 0, 0, 0, 0};
   double mx = 0.0;
   long long tsum = 0;
-  for (int b = lane; b < nblk; b += 32) {
-    const double* fp = D.fpart + ((size_t)b * D.R + r) * FSQR_FPART;
-    double v[8];
+  // records lane, lane + 32, ... in that order; two per lane per round, every load of a round issued
+  // before the first add (one memory latency per 64 records)
+  for (int bb = 0; bb < nblk; bb += 64) {
+    double v[2][8];
+    long long ts[2];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = __ldcg(fp + q);
-    const long long ts = __ldcg(D.ftsum + (size_t)b * D.R + r);
+    for (int u = 0; u < 2; ++u) {
+      const int b = bb + 32 * u + lane;
+      const bool ok = b < nblk;
+      const double* fp = D.fpart + ((size_t)(ok ? b : 0) * D.R + r) * FSQR_FPART;
 #pragma unroll
-    for (int q = 0; q < 7; ++q) a[q] += v[q];
-    mx = (v[7] > mx || !isfinite(v[7])) ? v[7] : mx;
-    tsum += ts;
+      for (int q = 0; q < 8; ++q) v[u][q] = ok ? __ldcg(fp + q) : 0.0;
+      ts[u] = ok ? __ldcg(D.ftsum + (size_t)b * D.R + r) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (bb + 32 * u + lane >= nblk) break;
+#pragma unroll
+      for (int q = 0; q < 7; ++q) a[q] += v[u][q];
+      mx = (v[u][7] > mx || !isfinite(v[u][7])) ? v[u][7] : mx;
+      tsum += ts[u];
+    }
   }
   const double dprev = D.delta[r];
 #pragma unroll
@@ -290,7 +303,7 @@ __device__ __forceinline__ bool fin_reduce_warp(const Dev& D, int r, int nblk, d
   const double rp = sqrt(a[0]) / (1.0 + sqrt(a[6]));
   const double rz = sqrt(a[3]) / (1.0 + sqrt(a[1]) + sqrt(a[2]));
   const double dnew = !requant ? dprev : (live ? ldexp(1.0, e_new - 28) : 1.0);
-  if (lane == 0) {
+  if (commit && lane == 0) {
     double* sc = D.scal + r * FSQR_NSCAL;
     sc[0] = rp;
     sc[1] = rz;
@@ -317,18 +330,22 @@ __device__ __forceinline__ void fin_requant(const Dev& D, int r, int t, int bar,
 
 // every active RHS's records: warp w of the group reduces RHS w, w + 8, ...; then the rare
 // re-quantisations, group-wide.  b0 per RHS from the state before this call (beta^k, sum theta^k).
-__device__ __forceinline__ void fin_reduce_all(const Dev& D, int nblk, long long k, int t, int bar, long long* smll) {
+// commit = false: the same code path without any store (a dry run that warms the instruction cache
+// of a CTA that will reduce once the records are complete).
+__device__ __forceinline__ void fin_reduce_all(const Dev& D, int nblk, long long k, int t, int bar, long long* smll,
+                                               bool commit = true) {
   __shared__ unsigned s_req;
   const int lane = t & 31, wid = t >> 5;
   if (t == 0) s_req = 0u;
   grp_bar(bar);
   for (int r = wid; r < D.R; r += FG / 32) {
-    if (D.status[r] != ST_ACTIVE) continue;
+    const int st = D.status[r];
     const double b0 = D.beta[(int)(k & 1)][r] + D.sumth[r] / D.eta[0];   // E14 with lambda_0 = 0, g_0 = sum theta^k
-    if (fin_reduce_warp(D, r, nblk, b0, k, lane) && lane == 0) atomicOr(&s_req, 1u << r);
+    if (st != ST_ACTIVE) continue;
+    if (fin_reduce_warp(D, r, nblk, b0, k, lane, commit) && lane == 0) atomicOr(&s_req, 1u << r);
   }
   grp_bar(bar);
-  const unsigned req = s_req;
+  const unsigned req = commit ? s_req : 0u;
   for (int r = 0; r < D.R; ++r)
     if (req & (1u << r)) fin_requant(D, r, t, bar, smll);
 }

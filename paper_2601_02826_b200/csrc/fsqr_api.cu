@@ -149,6 +149,9 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
+// column stride of an owned 2-bit copy (FSQR_DESIGN_PACK2): ceil(n/4) bytes rounded up to 128
+int64_t pack2_ld(int64_t n) { return ((n + 3) / 4 + 127) / 128 * 128; }
+
 fsqr_status make_tmaps(fsqr_ctx* ctx) {
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
@@ -158,7 +161,8 @@ fsqr_status make_tmaps(fsqr_ctx* ctx) {
   const Dev& D = ctx->D;
   {
     // u8: inner extent n samples; 2-bit: the packed column (ld bytes, zero padding beyond n/4)
-    cuuint64_t dims[2] = {(cuuint64_t)(D.storage == 2 ? D.ld : D.n), (cuuint64_t)D.p};
+    cuuint64_t dims[2] = {(cuuint64_t)(D.storage == 2 ? std::min<int64_t>(D.ld, ((D.n + 3) / 4 + 15) / 16 * 16) : D.n),
+                          (cuuint64_t)D.p};
     cuuint64_t strides[1] = {(cuuint64_t)D.ld};
     cuuint32_t box[2] = {128, 128};
     cuuint32_t es[2] = {1, 1};
@@ -501,7 +505,10 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
   if (X->flags & FSQR_DESIGN_PACK2) {
     // owned 2-bit copy of the u8 codes; everything below sees PACKED2 storage
     if (X->storage != FSQR_U8) return set_err(ctx, FSQR_ERR_CONFIG, "FSQR_DESIGN_PACK2 needs U8 storage");
-    const int64_t ld2 = (((X->n + 3) / 4 + 15) / 16) * 16;
+    // column stride a multiple of 128 bytes: every TMA box row of K2 and every 512-byte row-slab
+    // segment of the forward product is then one aligned line run (no straddled sectors); K2's
+    // tensor map still ends at round_up(n/4, 16), so the padding is never streamed
+    const int64_t ld2 = pack2_ld(X->n);
     uint8_t* x2;
     int* bad2;
     AL(x2, ld2 * X->p);
@@ -1483,7 +1490,7 @@ fsqr_status fsqr_fit_host(const fsqr_design* Xh, const double* y_host, int32_t n
       Xh->p >= 1 && Xh->ld >= Xh->n && Xh->ld % 16 == 0) {
     // u8 codes repacked on the way in: 256 MB column chunks are copied into a staging buffer and
     // packed straight into the 2-bit design, so only n*p/4 bytes of X are ever resident
-    const int64_t ld2 = ((Xh->n + 3) / 4 + 15) / 16 * 16;
+    const int64_t ld2 = pack2_ld(Xh->n);
     const int64_t cc = std::max<int64_t>(1, std::min<int64_t>(Xh->p, ((int64_t)256 << 20) / Xh->ld));
     uint8_t* stg = nullptr;
     int* bad = nullptr;

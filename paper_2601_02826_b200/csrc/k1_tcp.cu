@@ -144,7 +144,7 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
 // the forward accumulators and the colsum term are on the critical path.  Called by all threads.
 template <int NB>
 __device__ __forceinline__ void fused_records(const Dev& D, long long kit, int R, int nblk, int q0, int q1, int t,
-                                              int wid, int tid, double* smd) {
+                                              int wid, int tid, double* smd, unsigned nct) {
   FinRows<NB> pre;
   FinRHS pc;
   if (wid >= 4 && q0 < q1) {
@@ -154,7 +154,7 @@ __device__ __forceinline__ void fused_records(const Dev& D, long long kit, int R
       pc = fin_rhs(D, r, kit, 0);
     }
   }
-  // grid barrier: the grid is one CTA per SM and fully co-resident
+  // barrier of the nct product CTAs: the grid is one CTA per SM and fully co-resident
   fence_acq_rel_gpu();
   __syncthreads();
   if (tid == 0) {
@@ -162,7 +162,7 @@ __device__ __forceinline__ void fused_records(const Dev& D, long long kit, int R
     unsigned v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(D.k1bar) : "memory");
-    } while (v < gridDim.x);
+    } while (v < nct);
   }
   __syncthreads();
   if (wid < 4) return;
@@ -250,16 +250,20 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
   const bool stopped = *D.stop != 0;
   const bool skip = stopped || cnt == 0 || (K1P_DBG & 16);
   const bool fused = !cur;   // iteration mode: this kernel also runs the finalize (fin_common.cuh)
+  // fused: the last CTA is the REDUCER (no product items, no records): it waits for every product
+  // CTA's records and reduces them, its code already warm; the other nct CTAs do the product
+  const int nct = fused && gridDim.x > 1 ? (int)gridDim.x - 1 : (int)gridDim.x;
+  const bool reducer = (int)blockIdx.x >= nct;
   const int R = D.R;
   const int nslab = (D.n + SR - 1) / SR;
   // entries per work item: about one item per CTA, at most 2^16 (int32 digit sums stay exact:
   // |code 4^q| <= 192, |digit| <= 128, 192 * 128 * 2^16 < 2^31)
-  const int per = max(1, (int)gridDim.x / nslab);
+  const int per = max(1, nct / nslab);
   int64_t es = ((int64_t)max(cnt, 1) + per - 1) / per;
   // (u8 codes up to 255: 255 * 128 * 2^15 < 2^31, so at most 2^15 entries per item there)
   es = min((int64_t)min(D.k1_esmax, ST == 1 ? 32768 : 65536), ((es + KC - 1) / KC) * KC);
   const int64_t nsl = ((int64_t)cnt + es - 1) / es;
-  const int64_t nwork = skip ? 0 : nsl * nslab;
+  const int64_t nwork = (skip || reducer) ? 0 : nsl * nslab;
 
   if (wid == 0) {
     // ===================== producer: lane = support entry of the chunk
@@ -277,7 +281,7 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
     int bst = 0;
     uint32_t bph = 0;
     long long mbc = 0;   // metadata blocks used so far (buffer mbc & 1, parity (mbc >> 1) & 1)
-    for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+    for (int64_t w = blockIdx.x; w < nwork; w += nct) {
       const int slab = (int)(w % nslab);
       const int64_t e0 = (w / nslab) * es, e1 = min((int64_t)cnt, e0 + es);
       const int64_t nb = (e1 - e0 + MB - 1) / MB;
@@ -353,7 +357,7 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
     const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB);
     int bst = 0, ab = 0;
     uint32_t bph = 0, aphase = 0, tph = 0;
-    for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+    for (int64_t w = blockIdx.x; w < nwork; w += nct) {
       const int64_t e0 = (w / nslab) * es, e1 = min((int64_t)cnt, e0 + es);
       mbar_wait(tempty, tph ^ 1);
       tc_fence_after();
@@ -397,12 +401,15 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
     int ab = 0;
     uint32_t aphase = 0, tph = 0;
     long long ga = 0;   // u8: chunks handed to the MMA so far (A-buffer ring position)
-    for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+    for (int64_t w = blockIdx.x; w < nwork; w += nct) {
       const int slab = (int)(w % nslab);
       const int64_t e0 = (w / nslab) * es, e1 = min((int64_t)cnt, e0 + es);
       const int64_t nch = (e1 - e0 + KC - 1) / KC;
       const int64_t boff = (int64_t)slab * SEGB;
-      const int bytes = (int)min((int64_t)SEGB, D.ld - boff);
+      // bytes of this slab's segment that hold samples (2-bit: up to the 32-byte sector holding the
+      // last one; the column padding beyond it is never fetched)
+      const int64_t dw = ST == 1 ? D.ld : min(D.ld, (int64_t)((D.n + 3) / 4 + 31) / 32 * 32);
+      const int bytes = (int)min((int64_t)SEGB, dw - boff);
       const uint8_t* xs = D.X8 + boff;
       // my columns of chunk c: entries e0 + 32c + 4cw + kk, kk < 4 (-1 past the end).  Lane l holds
       // them for chunk 32 b + l of batch b (bi: the batch of the chunk being issued, bn: the next),
@@ -585,7 +592,7 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
   }
   if (!fused || stopped) return;
 #if K1P_TIMING
-  unsigned long long ts1, ts2, ts3, ts4;
+  unsigned long long ts1;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts1));
 #endif
 
@@ -593,62 +600,75 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
   double* smd = (double*)sA;
   long long* smll = (long long*)(smd + 4 * 8 * 9);
   const int nblk = (D.n + FG - 1) / FG;
-  const int tot = R * nblk, rper = (tot + (int)gridDim.x - 1) / (int)gridDim.x;
-  const int q0 = min(tot, (int)blockIdx.x * rper), q1 = min(tot, q0 + rper);
   const int t = tid - 128;
-  if (rper == 1) fused_records<1>(D, kit, R, nblk, q0, q1, t, wid, tid, smd);
-  else fused_records<4>(D, kit, R, nblk, q0, q1, t, wid, tid, smd);
-  // ticket: the last CTA reduces every RHS's records in fixed order and ends the iteration
-  __shared__ bool s_last;
+  if (!reducer) {
+    const int tot = R * nblk, rper = (tot + nct - 1) / nct;
+    const int q0 = min(tot, (int)blockIdx.x * rper), q1 = min(tot, q0 + rper);
+    if (rper == 1) fused_records<1>(D, kit, R, nblk, q0, q1, t, wid, tid, smd, (unsigned)nct);
+    else fused_records<4>(D, kit, R, nblk, q0, q1, t, wid, tid, smd, (unsigned)nct);
+    // publish this CTA's records to the reducer
 #if K1P_TIMING
-  ts2 = ts1;
-  unsigned long long ts2b, ts2c;
-  __syncthreads();
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts2b));
+    __syncthreads();
+    unsigned long long ts2b;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts2b));
 #endif
-  fence_acq_rel_gpu();
-  __syncthreads();
+    fence_acq_rel_gpu();
+    __syncthreads();
+    if (tid == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(D.fticket) : "memory");
 #if K1P_TIMING
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts2c));
+    unsigned long long ts3;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts3));
+    if (tid == 0 && kit == K1P_TIMING) {
+      unsigned long long* st = D.tstamp + 8 * blockIdx.x;
+      st[0] = ts0; st[1] = ts1; st[2] = ts1; st[3] = ts2b; st[4] = ts3; st[5] = ts3;
+      st[6] = (unsigned long long)__smid();
+      st[7] = (unsigned long long)((nwork - blockIdx.x + nct - 1) / nct);
+    }
 #endif
-  if (tid == 0) s_last = atomicAdd(D.fticket, 1u) == gridDim.x - 1;
-  __syncthreads();
-#if K1P_TIMING
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts3));
-  if (tid == 0 && kit == K1P_TIMING) {
-    unsigned long long* st = D.tstamp + 8 * blockIdx.x;
-    st[0] = ts0; st[1] = ts1; st[2] = ts2; st[3] = ts2b; st[4] = ts2c; st[5] = ts3;
-    st[6] = (unsigned long long)__smid() | ((unsigned long long)s_last << 32);
-    st[7] = (unsigned long long)((nwork - blockIdx.x + gridDim.x - 1) / gridDim.x);
+    return;
   }
-#endif
-  if (!s_last || wid < 4) return;
-  fence_acq_rel_gpu();
+  if (wid < 4) return;
+  // reducer: a dry run of the reduction (no stores) while the records are being written, so that
+  // the committed pass runs from a warm instruction cache; then wait for all nct tickets
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) {
+      if (t == 0) {
+        unsigned v;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(D.fticket) : "memory");
+        } while (v < (unsigned)nct);
+      }
+      grp_bar(1);
+      fence_acq_rel_gpu();
 #if K1P_TIMING
-  unsigned long long tq0;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tq0));
-  if (t == 0 && kit == K1P_TIMING) D.tstamp[8 * 148 + 70] = tq0;
+      if (t == 0 && kit == K1P_TIMING) {
+        unsigned long long tq0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tq0));
+        D.tstamp[8 * 148 + 70] = tq0;
+      }
 #endif
-#if K1P_TIMING
-  long long cy0 = clock64();
-#endif
-  fin_reduce_all(D, nblk, kit, t, 1, smll);
-#if K1P_TIMING
-  {
-    long long dep = 0;
-    asm volatile("mov.u64 %0, 0;" : "=l"(dep) : "d"(D.delta[0]));
-    if (t == 0 && kit == K1P_TIMING) D.tstamp[8 * 148 + 74] = (unsigned long long)(clock64() + dep - cy0);
+    }
+    fin_reduce_all(D, nblk, kit, t, 1, smll, pass == 1);
   }
-#endif
   if (t < R) D.mterm[t] = 0;
   fin_iteration_tail(D, kit, t);
   if (t == 0) {
     *D.fticket = 0u;
-    *D.k1bar = 0u;   // every CTA has left the barrier (each took a ticket after it)
+    *D.k1bar = 0u;   // every product CTA has left the barrier (each published its records after it)
   }
 #if K1P_TIMING
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts4));
-  if (t == 0 && kit == K1P_TIMING) D.tstamp[8 * 148 + 40] = ts4;
+  {
+    unsigned long long ts4;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts4));
+    if (t == 0 && kit == K1P_TIMING) {
+      D.tstamp[8 * 148 + 40] = ts4;
+      unsigned long long* st = D.tstamp + 8 * blockIdx.x;
+      st[0] = ts0; st[1] = ts1; st[2] = ts1; st[3] = ts1; st[4] = ts1; st[5] = ts1;
+      st[6] = (unsigned long long)__smid() | (1ull << 32);
+      st[7] = 0;
+    }
+  }
 #endif
 }
 

@@ -27,24 +27,10 @@ torch.cuda.synchronize()
 st = fs.fsqr_debug_stamps(S.ctx).astype('int64')
 cta = st[:8 * 148].reshape(148, 8)
 t0 = cta[:, 0].min()
-names = ["start", "itemsdone", "barrier", "recwork", "fence", "ticket"]
+prod = cta[(cta[:, 6] >> 32) == 0]
+names = ["start", "itemsdone", "barrier", "recdone", "published"]
 for k, nm in enumerate(names):
-    v = (cta[:, k] - t0) / 1000.0
+    v = (prod[:, k] - t0) / 1000.0
     print(f"{nm:10s} min {v.min():7.2f} med {statistics.median(v):7.2f} max {v.max():7.2f} us")
-print("reduce (before requant) %.2f us, requant %d" % ((st[8 * 148 + 50] - t0) / 1e3, st[8 * 148 + 51]))
-print("reduce_rhs0 done %.2f us, tail end %.2f us" % ((st[8 * 148] - t0) / 1e3, (st[8 * 148 + 40] - t0) / 1e3))
-slow = sorted(range(148), key=lambda c: -cta[c, 4])[:10]
-print("slowest fences (cta, sm, us):", [(c, int(cta[c, 6] & 0xffffffff), round((cta[c, 4] - t0) / 1e3, 2)) for c in slow])
-
-rec = st[1300:1300 + 4 * 40].reshape(40, 4)
-for nm, k in (("rec start", 0), ("loads done", 1), ("rows+warp red", 2), ("group bar", 3)):
-    v = (rec[:, k] - t0) / 1e3
-    print(f"{nm:14s} min {v.min():7.2f} med {statistics.median(v):7.2f} max {v.max():7.2f} us")
-
-lc = st[8 * 148:8 * 148 + 80]
-print("last CTA: after fence %.2f, reduced %.2f us (requant mask %d)" % (
-    (lc[70] - t0) / 1e3, (st[1234] - t0) / 1e3, st[1235]))
-print("warp reduce of RHS 0: loads done %.2f, butterfly done %.2f, scalars done %.2f us" % tuple((st[1234 + q] - t0) / 1e3 for q in (20, 21, 22)))
-cyc = st[8 * 148 + 200: 8 * 148 + 200 + 148]
-print("record phase cycles per CTA (records CTAs): min %d med %d max %d" % (cyc[cyc > 0].min(), np.median(cyc[cyc > 0]), cyc.max()))
-print("last CTA fin_reduce_all cycles: %d" % st[8 * 148 + 74])
+print("reducer: records complete %.2f us, iteration done %.2f us" % ((st[8 * 148 + 70] - t0) / 1e3,
+                                                                     (st[8 * 148 + 40] - t0) / 1e3))
