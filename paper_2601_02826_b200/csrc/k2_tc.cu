@@ -181,7 +181,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
       const int acc = lt & 1;
       const uint32_t aph = (lt >> 1) & 1;
-      mbar_wait(&tfull[acc], aph);
+      epi_prefetch<RMAX>(D, C, (t + (int64_t)gridDim.x) * TILE_M + q * 32 + lane);
+      mbar_wait_park(&tfull[acc], aph);
       tc_fence_after();
       int32_t dv[NPAD];
 #pragma unroll

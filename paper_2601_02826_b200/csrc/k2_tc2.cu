@@ -36,6 +36,9 @@
 #ifndef K2TC2_BATOMS
 #define K2TC2_BATOMS 4   // theta-digit atoms loaded per stage (4; fewer only in measurement variants)
 #endif
+#ifndef K2TC2_L2PF
+#define K2TC2_L2PF 20   // k-blocks of the next pass's first tile prefetched into L2 at the end of a pass (0: off)
+#endif
 #ifndef K2TC2_CW
 #define K2TC2_CW 8   // converter warps (two per SM sub-partition: the unpack loop is latency-bound with one)
 #endif
@@ -226,6 +229,18 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
           }
         }
       }
+      // every load of this pass is issued: pull the first K2TC2_L2PF k-blocks of this CTA's first
+      // tiles of the NEXT pass (X does not change) into L2 while the forward product and the finalize
+      // run (HBM is nearly idle then), so the next pass starts from L2 instead of waiting on HBM
+      if (D.update && elect_one()) {
+        const uint64_t pol_pf = policy_evict_normal();
+        for (int i = 0; i < K2TC2_L2PF; ++i) {
+          const int64_t tt = blockIdx.x + (int64_t)(i / kblocks) * gridDim.x;
+          if (tt >= ntiles) break;
+          tma_prefetch_l2(&tmX, (i % kblocks) * PK, (int)(tt * TILE_M), pol_pf);
+        }
+      }
+      __syncwarp();
     }
   } else if (wid == 1) {
     // ===== MMA issuer: the whole warp walks the pipeline, one elected lane issues =====
@@ -339,7 +354,8 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
       const int acc = lt & 1;
       if (CF::EW == 8 && acc != eset) continue;
       const uint32_t aph = (lt >> 1) & 1;
-      mbar_wait(&tfull[acc], aph);
+      epi_prefetch<RMAX>(D, C, (t + (int64_t)gridDim.x * (CF::EW == 8 ? 2 : 1)) * TILE_M + q * 32 + lane);
+      mbar_wait_park(&tfull[acc], aph);
       tc_fence_after();
       int32_t dv[NPAD];
       if constexpr (CF::SPLITQ) {

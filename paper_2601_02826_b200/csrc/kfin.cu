@@ -441,6 +441,11 @@ __global__ void k_back_f64(const Dev D, const double* u, int per_block, const in
 
 // ---- genotype-storage power / lambda_max products (a0', R3-R4): 16 rows per thread, vector loads
 
+// a small unsigned integer as a double without the quarter-rate I2F.F64: (2^52 + c) - 2^52, exact
+__device__ __forceinline__ double code_to_double(uint32_t c) {
+  return __hiloint2double(0x43300000, (int)c) - 4503599627370496.0;
+}
+
 // codes of rows i0..i0+15 of data column c (u8: one 16-byte load; 2-bit: one 4-byte load)
 template <int ST>
 __device__ __forceinline__ void codes16(const Dev& D, int64_t c, int i0, double (&x)[16]) {
@@ -448,11 +453,11 @@ __device__ __forceinline__ void codes16(const Dev& D, int64_t c, int i0, double 
     const uint4 v = __ldcs((const uint4*)(D.X8 + c * D.ld + i0));
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int q = 0; q < 16; ++q) x[q] = (double)((w[q >> 2] >> (8 * (q & 3))) & 0xFFu);
+    for (int q = 0; q < 16; ++q) x[q] = code_to_double((w[q >> 2] >> (8 * (q & 3))) & 0xFFu);
   } else {
     const uint32_t w = __ldcs((const uint32_t*)(D.X8 + c * D.ld + (i0 >> 2)));
 #pragma unroll
-    for (int q = 0; q < 16; ++q) x[q] = (double)((w >> (2 * q)) & 3u);
+    for (int q = 0; q < 16; ++q) x[q] = code_to_double((w >> (2 * q)) & 3u);
   }
 }
 
@@ -525,13 +530,26 @@ __global__ void __launch_bounds__(256) k_back_int(const Dev D, const double* u, 
     double acc = 0.0;
     const int64_t c = j >= 1 ? j - 1 : 0;
     if (live && j >= 1) {
-      for (int i0 = 0; i0 < D.n; i0 += 16) {
-        double x[16];
-        codes16<ST>(D, c, i0, x);
-        const int lim = min(16, D.n - i0);
+      if (ST == 2) {
+        // 64 rows per 16-byte load (the column stride and i0 / 4 are multiples of 16 bytes; the
+        // bytes past n / 4 are zero padding), rows in order: the same sum as 16 at a time
+        for (int i0 = 0; i0 < D.n; i0 += 64) {
+          const uint4 v = __ldg((const uint4*)(D.X8 + c * D.ld + (i0 >> 2)));
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+          const int lim = min(64, D.n - i0);
 #pragma unroll
-        for (int q = 0; q < 16; ++q)
-          if (q < lim) acc = fma(x[q], __ldg(ug + i0 + q), acc);
+          for (int q = 0; q < 64; ++q)
+            if (q < lim) acc = fma(code_to_double((w[q >> 4] >> (2 * (q & 15))) & 3u), __ldg(ug + i0 + q), acc);
+        }
+      } else {
+        for (int i0 = 0; i0 < D.n; i0 += 16) {
+          double x[16];
+          codes16<ST>(D, c, i0, x);
+          const int lim = min(16, D.n - i0);
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (q < lim) acc = fma(x[q], __ldg(ug + i0 + q), acc);
+        }
       }
     }
     if (live) {
