@@ -38,6 +38,10 @@ void launch_lanczos_orth(const Dev& D, const double* v, const double* vp, double
 void launch_lanczos_next(const Dev& D, double* v, double* vp, const double* w, const double* beta, const int* frozen,
                          cudaStream_t st);
 void launch_null_score(const double* y, int n, const double* tau, int R, double* psi, cudaStream_t st);
+void launch_power_quant(const Dev& D, const double* u, const double* Ug, const int* frozen, int8_t* Bp, int ldk,
+                        long long* Tsum, double* gs, double* w, cudaStream_t st);
+void launch_power_back_tc2(const Dev& D, const void* tmX, const void* tmBp, const long long* Tsum, const double* gs,
+                           const int* frozen, double* w, int grid, cudaStream_t st);
 void launch_power_fwd_int(const Dev& D, const int64_t* bstart, const double* v, const int* frozen, double* part,
                           int S, double* u, double* Ug, cudaStream_t st);
 void launch_sum_parts(const double* part, int S, int G, int n, double* u, double* Ug, cudaStream_t st);
@@ -312,6 +316,39 @@ fsqr_status power_method(fsqr_ctx* ctx, cudaStream_t st) {
     AL(part, (size_t)S * G * D.n);
     AL(Ug, G);
   }
+  // back pass X~_g^T u_g on the tensor cores for 2-bit storage (k2p_kernel): u_g as int8 digit planes
+  // (rows 4g..4g+3 of Bp, plus 4 zero rows for the last block's pair); blocks of >= 128 columns keep
+  // every 128-column tile within two blocks.  Otherwise the CUDA-core k_back_int.
+  const bool tcback = ctx->backend == FSQR_BACKEND_TC && D.storage == FSQR_PACKED2 && D.gq >= 128;
+  int8_t* Bp = nullptr;
+  long long* Tsum = nullptr;
+  double* gsc = nullptr;
+  CUtensorMap tmBp{};
+  if (tcback) {
+    AL(Bp, (size_t)4 * (G + 1) * D.ldk);
+    AL(Tsum, G);
+    AL(gsc, G);
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return set_err(ctx, FSQR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)D.ldk, (cuuint64_t)(4 * (G + 1))};
+    cuuint64_t strides[1] = {(cuuint64_t)D.ldk};
+    cuuint32_t box[2] = {128, 8};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = ((EncodeTiledFn)fn)(&tmBp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)Bp, dims, strides, box, es,
+                                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(ctx, FSQR_ERR_CUDA, "tensor map for the power digits failed (%d)", (int)r);
+  }
+  auto back = [&](const double* uu, const double* ug, double* ww) {
+    if (tcback) {
+      launch_power_quant(D, uu, ug, d_frozen, Bp, D.ldk, Tsum, gsc, ww, st);
+      launch_power_back_tc2(D, &ctx->tmX, &tmBp, Tsum, gsc, d_frozen, ww, ctx->k2_grid, st);
+    } else {
+      launch_back_int(D, uu, ug, 1, d_frozen, ww, nullptr, st);
+    }
+  };
   CK(cudaMemcpyAsync(d_bs, bs.data(), sizeof(int64_t) * (G + 1), cudaMemcpyHostToDevice, st));
   launch_power_start(p1, ctx->opt.seed, v, st);
   launch_power_reduce(D, d_bs, v, v, d_frozen, est, nrm, st);
@@ -333,7 +370,7 @@ fsqr_status power_method(fsqr_ctx* ctx, cudaStream_t st) {
     for (int it = 1; it <= ctx->opt.power_max_iter && live > 0; ++it) {
       if (geno) {
         launch_power_fwd_int(D, d_bs, v, d_frozen, part, S, u, Ug, st);
-        launch_back_int(D, u, Ug, 1, d_frozen, w, nullptr, st);
+        back(u, Ug, w);
       } else {
         launch_power_fwd(D, d_bs, v, d_frozen, u, st);
         launch_back_f64(D, u, 1, d_frozen, w, nullptr, st);
@@ -369,7 +406,7 @@ fsqr_status power_method(fsqr_ctx* ctx, cudaStream_t st) {
   for (int it = 1; it <= ctx->opt.power_max_iter && live > 0; ++it) {
     if (geno) {
       launch_power_fwd_int(D, d_bs, v, d_frozen, part, S, u, Ug, st);
-      launch_back_int(D, u, Ug, 1, d_frozen, w, nullptr, st);
+      back(u, Ug, w);
     } else {
       launch_power_fwd(D, d_bs, v, d_frozen, u, st);
       launch_back_f64(D, u, 1, d_frozen, w, nullptr, st);
@@ -754,6 +791,10 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
       if (!std::isfinite(hy[i])) return set_err(ctx, FSQR_ERR_DATA, "y[%lld] is not finite", (long long)i);
   }
 
+  if (ctx->backend == FSQR_BACKEND_TC) {   // (the power method's tensor-core back pass streams X through tmX)
+    fsqr_status s = make_tmaps(ctx);
+    if (s != FSQR_OK) return s;
+  }
   // ---------------- a0': eta_g
   if (o.eta_host) {
     ctx->eta.assign(o.eta_host, o.eta_host + o.G);
@@ -777,10 +818,6 @@ static fsqr_status create_impl(fsqr_ctx* ctx, const fsqr_design* X, const double
   {
     std::vector<double> one(R, 1.0);
     CK(cudaMemcpyAsync(D.delta, one.data(), sizeof(double) * R, cudaMemcpyHostToDevice, st));
-  }
-  if (ctx->backend == FSQR_BACKEND_TC) {
-    fsqr_status s = make_tmaps(ctx);
-    if (s != FSQR_OK) return s;
   }
   {
     fsqr_status s = init_state(ctx, st);

@@ -37,7 +37,7 @@
 #define K2TC2_BATOMS 4   // theta-digit atoms loaded per stage (4; fewer only in measurement variants)
 #endif
 #ifndef K2TC2_L2PF
-#define K2TC2_L2PF 20   // k-blocks of the next pass's first tile prefetched into L2 at the end of a pass (0: off)
+#define K2TC2_L2PF 0    // k-blocks of the next pass's first tiles prefetched into L2 at the end of a pass (measured: 20 or 40 cost 2-3% at M, so off)
 #endif
 #ifndef K2TC2_CW
 #define K2TC2_CW 8   // converter warps (two per SM sub-partition: the unpack loop is latency-bound with one)
@@ -411,6 +411,229 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
   k2_finish<RMAX>(D, C, P, red);
 }
 
+// ---------------------------------------------------------------- power-method back pass (a0')
+// w_j = (X~_g^T u_g)_j for every model column j >= 1 of its block g (L259: the power / Lanczos
+// products for eta_g), on the same TMA -> TMEM-unpack -> tcgen05 pipeline: the B operand of a tile
+// is the int8 digit planes of u_g (28-bit fixed point per block, Bp rows 4g..4g+3, written by
+// k_power_quant in the converter's K order).  Blocks hold >= 128 columns (checked by the host), so a
+// 128-column tile touches blocks g0 and g0 + 1 at most and each stage loads their 8 digit rows.
+struct PowBack {
+  const long long* Tsum;   // [G] sum_i T_gi
+  const double* gs;        // [G] delta_g / n
+  const int* frozen;       // [G]
+  double* w;               // [p + 1]
+};
+
+__global__ void __launch_bounds__(Cfg2<16, 1>::THREADS, 1)
+    k2p_kernel(const Dev D, const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmBp,
+               const PowBack PB) {
+  using CF = Cfg2<16, 1>;
+  constexpr int NPAD = 16;
+  constexpr int CW = CF::CW;
+  constexpr int EPI0 = 4 + CW;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + (((1023 + 1) - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + CF::STAGES * A_BYTES;
+  uint64_t* full = (uint64_t*)(smem + CF::STAGES * CF::STAGE);
+  uint64_t* empty = full + CF::STAGES;
+  uint64_t* afull = empty + CF::STAGES;
+  constexpr int NAB = CF::NAB, A_COL0 = CF::A_COL0;
+  uint64_t* aempty = afull + NAB;
+  uint64_t* tfull = aempty + NAB;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int64_t ntiles = (D.p + TILE_M - 1) / TILE_M;
+  const int kblocks = (int)((D.ld + PK - 1) / PK);
+  if (wid == 0 && lane == 0) {
+    prefetch_tmap(&tmX);
+    prefetch_tmap(&tmBp);
+    for (int s = 0; s < CF::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < NAB; ++a) {
+      mbar_init(&afull[a], CW);
+      mbar_init(&aempty[a], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+  }
+  if (wid == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  // digit rows 8..15 of every B stage are never loaded (the box has 8 rows): zero them once
+  for (int s = 0; s < CF::STAGES; ++s)
+    for (int a = 0; a < 4; ++a) {
+      uint8_t* base = sB + s * CF::B_BYTES + a * NPAD * 128;
+      for (int q = 8 * 128 + tid * 16; q < NPAD * 128; q += CF::THREADS * 16) *(uint4*)(base + q) = make_uint4(0, 0, 0, 0);
+    }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (wid == 0) {
+    const uint64_t pol_x = policy_evict_first(), pol_b = policy_evict_last();
+    const uint32_t bytes = (uint32_t)(A_BYTES + 4 * 8 * 128);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int g0 = block_of_col(D, t * TILE_M + 1);
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (elect_one()) {
+          mbar_expect_tx(&full[stage], bytes);
+          tma_load_2d(sA + stage * A_BYTES, &tmX, &full[stage], kb * PK, (int)(t * TILE_M), pol_x);
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+            tma_load_2d(sB + stage * CF::B_BYTES + a * CF::B_ATOM, &tmBp, &full[stage], kb * KS + a * 128, 4 * g0, pol_b);
+        }
+        __syncwarp();
+        if (++stage == CF::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (wid == 1) {
+    constexpr uint32_t idesc = idesc_u8s8(NPAD);
+    const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
+    const uint32_t sB0 = smem_u32(sB);
+    int stage = 0, ab = 0;
+    uint32_t phase = 0, aphase = 0;
+    int lt = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+      const int acc = lt & 1;
+      mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tbase + (uint32_t)(acc * CF::ACC_COLS);
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        mbar_wait(&afull[ab], aphase);
+        tc_fence_after();
+        const uint32_t a_tmem = tbase + (uint32_t)(A_COL0 + ab * A_COLS);
+        const uint64_t bdesc0 = umma_desc_sw128(sB0 + (uint32_t)(stage * CF::B_BYTES));
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < KS / 32; ++kk)
+            umma_i8_tmem_a(d_tmem + (uint32_t)((kk >> 2) * NPAD), a_tmem + (uint32_t)(8 * kk),
+                           bdesc0 + (uint64_t)((kk >> 2) * (CF::B_ATOM >> 4) + 2 * (kk & 3)), idesc,
+                           (kb != 0 || (kk & 3) != 0) ? 1u : 0u);
+          umma_commit(&empty[stage]);
+          umma_commit(&aempty[ab]);
+        }
+        __syncwarp();
+        if (++stage == CF::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+        if (++ab == NAB) {
+          ab = 0;
+          aphase ^= 1;
+        }
+      }
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
+    }
+  } else if (wid >= 4 && wid < EPI0) {
+    // converters: identical to k2_tc2_kernel<16, 1> (codes left in place, one plane per accumulator)
+    constexpr int CH = 8 / (CW / 4);
+    constexpr int NW = 4 * CH;
+    static_assert(NW == 16, "eight converter warps");
+    const int q4 = wid & 3;
+    const int h = (wid - 4) >> 2;
+    const int c = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    int stage = 0, ab = 0;
+    uint32_t phase = 0, aphase = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        mbar_wait(&aempty[ab], aphase ^ 1);
+        tc_fence_after();
+        uint32_t w[NW];
+        const uint8_t* row = sA + stage * A_BYTES + c * PK;
+#pragma unroll
+        for (int jj = 0; jj < CH; ++jj) {
+          const int j = h * CH + jj;
+          const uint4 v = *(const uint4*)(row + ((j ^ (c & 7)) << 4));
+          w[4 * jj] = v.x;
+          w[4 * jj + 1] = v.y;
+          w[4 * jj + 2] = v.z;
+          w[4 * jj + 3] = v.w;
+        }
+        const uint32_t abase = tmem_base + lane_off + (uint32_t)(A_COL0 + ab * A_COLS + h * NW);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t o[NW];
+#pragma unroll
+          for (int u = 0; u < NW; ++u) o[u] = w[u] & (0x03030303u << (2 * q));
+          tmem_st16(abase + (uint32_t)(32 * q), o);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&afull[ab]);
+        if (++stage == CF::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+        if (++ab == NAB) {
+          ab = 0;
+          aphase ^= 1;
+        }
+      }
+    }
+  } else if (wid >= EPI0) {
+    const int q = wid & 3;
+    int lt = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+      const int acc = lt & 1;
+      mbar_wait_park(&tfull[acc], (lt >> 1) & 1);
+      tc_fence_after();
+      int32_t dv[NPAD];
+#pragma unroll
+      for (int u = 0; u < NPAD; ++u) dv[u] = 0;
+#pragma unroll
+      for (int pq = 0; pq < 4; ++pq) {
+        uint32_t v[16];
+        tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * CF::ACC_COLS + pq * NPAD), v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 16; ++u) dv[u] += ((int32_t)v[u]) >> (2 * pq);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      const int64_t c = t * TILE_M + q * 32 + lane;
+      if (c < D.p) {
+        const int g0 = block_of_col(D, t * TILE_M + 1), g = block_of_col(D, c + 1);
+        if (!PB.frozen[g]) {
+          const int sl = (g - g0) & 1;
+          const int32_t* Dk = dv + 4 * sl;
+          PB.w[c + 1] = g_from_digits(D.n, D.colsum[c], PB.Tsum[g], PB.gs[g], D.inv_sd[c], Dk);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (wid == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
+  }
+}
+
 template <int NPAD, int RM>
 void launch_np(const Dev& D, const void* tmX, const void* tmB, int grid, cudaStream_t st) {
   launch_pdl(k2_tc2_kernel<NPAD, RM>, dim3(grid), dim3(Cfg2<NPAD, RM>::THREADS), Cfg2<NPAD, RM>::SMEM, st, D,
@@ -427,6 +650,9 @@ cudaError_t init_np() {
 
 cudaError_t k2_tc2_init() {
   cudaError_t e;
+  if ((e = cudaFuncSetAttribute(k2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<16, 1>::SMEM)) !=
+      cudaSuccess)
+    return e;
   if ((e = init_np<16, 1>()) != cudaSuccess) return e;
   if ((e = init_np<16, 4>()) != cudaSuccess) return e;
   if ((e = init_np<32, 8>()) != cudaSuccess) return e;
@@ -440,4 +666,11 @@ void launch_k2_tc2(const Dev& D, const void* tmX, const void* tmB, int grid, cud
   else if (D.npad == 32) launch_np<32, 8>(D, tmX, tmB, grid, st);
   else if (D.npad == 48) launch_np<48, 12>(D, tmX, tmB, grid, st);
   else launch_np<64, 16>(D, tmX, tmB, grid, st);
+}
+
+void launch_power_back_tc2(const Dev& D, const void* tmX, const void* tmBp, const long long* Tsum, const double* gs,
+                           const int* frozen, double* w, int grid, cudaStream_t st) {
+  const PowBack PB{Tsum, gs, frozen, w};
+  k2p_kernel<<<grid, Cfg2<16, 1>::THREADS, Cfg2<16, 1>::SMEM, st>>>(D, *(const CUtensorMap*)tmX, *(const CUtensorMap*)tmBp,
+                                                                   PB);
 }

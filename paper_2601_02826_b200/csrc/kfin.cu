@@ -476,19 +476,42 @@ __global__ void __launch_bounds__(128) k_power_fwd_int(const Dev D, const int64_
 #pragma unroll
   for (int q = 0; q < 16; ++q) acc[q] = 0.0;
   double cterm = 0.0;
-  for (int64_t j = a0; j < a1; ++j) {
-    const double vj = v[j];
-    if (j == 0) {
-      cterm -= vj;
-      continue;
-    }
-    const int64_t c = j - 1;
-    const double a = D.inv_sd[c] * vj;
-    cterm = fma(D.mean[c], a, cterm);
-    double x[16];
-    codes16<ST>(D, c, i0, x);
+  // four columns per step with every load issued first (the per-column scalars and codes are
+  // otherwise one memory latency per column); the sums keep the column order
+  constexpr int U = 4;
+  for (int64_t jb = a0; jb < a1; jb += U) {
+    double vj[U], isd[U], mn[U];
+    uint4 cw[U];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) acc[q] = fma(x[q], a, acc[q]);
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = jb + u;
+      const bool ok = j < a1 && j >= 1;
+      const int64_t c = ok ? j - 1 : 0;
+      vj[u] = j < a1 ? v[j] : 0.0;
+      isd[u] = ok ? D.inv_sd[c] : 0.0;
+      mn[u] = ok ? D.mean[c] : 0.0;
+      if (ST == 1) cw[u] = ok ? __ldcs((const uint4*)(D.X8 + c * D.ld + i0)) : make_uint4(0, 0, 0, 0);
+      else cw[u].x = ok ? __ldcs((const uint32_t*)(D.X8 + c * D.ld + (i0 >> 2))) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = jb + u;
+      if (j >= a1) break;
+      if (j == 0) {
+        cterm -= vj[u];
+        continue;
+      }
+      const double a = isd[u] * vj[u];
+      cterm = fma(mn[u], a, cterm);
+      if (ST == 1) {
+        const uint32_t w[4] = {cw[u].x, cw[u].y, cw[u].z, cw[u].w};
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc[q] = fma(code_to_double((w[q >> 2] >> (8 * (q & 3))) & 0xFFu), a, acc[q]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc[q] = fma(code_to_double((cw[u].x >> (2 * q)) & 3u), a, acc[q]);
+      }
+    }
   }
   double* out = part + ((int64_t)s * D.G + g) * D.n;
 #pragma unroll
@@ -557,6 +580,48 @@ __global__ void __launch_bounds__(256) k_back_int(const Dev D, const double* u, 
       if (w) w[j] = wj;
       if (maxbits && j >= 1) atomicMax(maxbits, (unsigned long long)__double_as_longlong(fabs(wj)));
     }
+  }
+}
+
+// per block g (one CTA each): u_g as 28-bit fixed point T_gi = round(u_gi / delta_g), delta_g =
+// 2^(e - 28) with e the binary exponent of max_i |u_gi|, split into four signed base-256 digits in
+// rows 4g..4g+3 of Bp (the tensor-core K order of bq_index), Tsum_g = sum_i T_gi, gs_g = delta_g / n;
+// and w_0 = sum_i u_0i for the intercept (block 0).  The back pass k2p_kernel reads them.
+__global__ void __launch_bounds__(FT) k_power_quant(const Dev D, const double* u, const double* Ug, const int* frozen,
+                                                    int8_t* Bp, int ldk, long long* Tsum, double* gs, double* w) {
+  __shared__ double smd[33];
+  __shared__ long long smll[33];
+  const int g = blockIdx.x;
+  if (frozen[g]) return;
+  const double* ug = u + (int64_t)g * D.n;
+  double mx = 0.0;
+  for (int i = threadIdx.x; i < D.n; i += blockDim.x) mx = fmax(mx, fabs(ug[i]));
+  mx = block_max(mx, smd);
+  int e = 0;
+  if (mx > 0.0 && isfinite(mx)) frexp(mx, &e);
+  const double delta = (mx > 0.0 && isfinite(mx)) ? ldexp(1.0, e - 28) : 1.0, inv = 1.0 / delta;
+  int8_t* b0 = Bp + (int64_t)(4 * g) * ldk;
+  long long ts = 0;
+  for (int i = threadIdx.x; i < D.n; i += blockDim.x) {
+    long long T = isfinite(ug[i]) ? __double2ll_rn(ug[i] * inv) : 0;
+    ts += T;
+    const int d3 = (int)(int8_t)(T & 0xFF);
+    T = (T - d3) >> 8;
+    const int d2 = (int)(int8_t)(T & 0xFF);
+    T = (T - d2) >> 8;
+    const int d1 = (int)(int8_t)(T & 0xFF);
+    T = (T - d1) >> 8;
+    const int ix = bq_index(D, i);
+    b0[ix] = (int8_t)T;
+    b0[ldk + ix] = (int8_t)d1;
+    b0[2 * ldk + ix] = (int8_t)d2;
+    b0[3 * ldk + ix] = (int8_t)d3;
+  }
+  ts = block_sum_ll(ts, smll);
+  if (threadIdx.x == 0) {
+    Tsum[g] = ts;
+    gs[g] = delta / (double)D.n;
+    if (g == 0) w[0] = Ug[0];
   }
 }
 
@@ -868,4 +933,8 @@ void launch_unfreeze(const Dev& D, cudaStream_t st) {
 }
 void launch_lla_weights(const Dev& D, int kind, double a, cudaStream_t st) {
   k_lla_weights<<<592, 256, 0, st>>>(D, kind, a);
+}
+void launch_power_quant(const Dev& D, const double* u, const double* Ug, const int* frozen, int8_t* Bp, int ldk,
+                        long long* Tsum, double* gs, double* w, cudaStream_t st) {
+  k_power_quant<<<D.G, FT, 0, st>>>(D, u, Ug, frozen, Bp, ldk, Tsum, gs, w);
 }

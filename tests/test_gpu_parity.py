@@ -38,6 +38,23 @@ def test_colstats_lambda_max_eta(cuda_ok, name, storage, method):
     np.testing.assert_allclose(S.eta(), eta_orc, rtol=1e-6)
 
 
+@pytest.mark.parametrize("method", ["lanczos", "power"])
+@pytest.mark.parametrize("flags", [0, 1])
+def test_eta_tensor_core_back_pass(cuda_ok, method, flags):
+    """eta_g (L259) with the power method's back pass X~_g^T u_g on the tensor cores (2-bit storage,
+    blocks of >= 128 columns: k_power_quant + k2p_kernel): G = 7 puts block boundaries inside 128-column
+    tiles, n = 1000 leaves a ragged K tail; 2-bit as stored (C4 recipe) and u8 repacked at create."""
+    import paper_2601_02826_b200 as fs
+
+    name, storage = ("c4", 2) if flags == 0 else ("c2", 1)
+    prob, d, S, cfg = make_pair(name, n=1000, p=3001, G=7, storage=storage, oracle_eta=False,
+                                eta_method=fs.ETA_LANCZOS if method == "lanczos" else fs.ETA_POWER,
+                                flags=fs.DESIGN_PACK2 if flags else 0)
+    assert S.backend == "tc"
+    eta_orc = oracle.eta(d, cfg["G"], cfg["mu"], method=method)
+    np.testing.assert_allclose(S.eta(), eta_orc, rtol=1e-6)
+
+
 @pytest.mark.parametrize("name,storage,n,p,backend", [
     ("c1", 0, 200, 2000, 2),          # dense fp32, configs[0] at full size
     ("c2", 1, 1000, 3001, 1),         # u8, tcgen05: ragged K tail (1000 % 128) and column tail (3001 % 128)
