@@ -260,6 +260,7 @@ __device__ __forceinline__ bool fin_reduce_warp(const Dev& D, int r, int nblk, d
   double a[7] = {0, 0, 0, 0, 0, 0, 0};
   double mx = 0.0;
   long long tsum = 0;
+  const double dprev = D.delta[r];   // issued with the record loads (one memory latency in all)
   // records lane, lane + 32, ... in that order; two per lane per round, every load of a round issued
   // before the first add (one memory latency per 64 records)
   for (int bb = 0; bb < nblk; bb += 64) {
@@ -283,7 +284,6 @@ __device__ __forceinline__ bool fin_reduce_warp(const Dev& D, int r, int nblk, d
       tsum += ts[u];
     }
   }
-  const double dprev = D.delta[r];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
@@ -339,10 +339,12 @@ __device__ __forceinline__ void fin_reduce_all(const Dev& D, int nblk, long long
   if (t == 0) s_req = 0u;
   grp_bar(bar);
   for (int r = wid; r < D.R; r += FG / 32) {
+    // status, beta_0, sum theta and the records are loaded together; an RHS that is not active
+    // (its records were not written this iteration) publishes nothing
     const int st = D.status[r];
     const double b0 = D.beta[(int)(k & 1)][r] + D.sumth[r] / D.eta[0];   // E14 with lambda_0 = 0, g_0 = sum theta^k
-    if (st != ST_ACTIVE) continue;
-    if (fin_reduce_warp(D, r, nblk, b0, k, lane, commit) && lane == 0) atomicOr(&s_req, 1u << r);
+    const bool act = st == ST_ACTIVE;
+    if (fin_reduce_warp(D, r, nblk, b0, k, lane, commit && act) && act && lane == 0) atomicOr(&s_req, 1u << r);
   }
   grp_bar(bar);
   const unsigned req = commit ? s_req : 0u;

@@ -154,10 +154,12 @@ __device__ __forceinline__ void fused_records(const Dev& D, long long kit, int R
       pc = fin_rhs(D, r, kit, 0);
     }
   }
-  // barrier of the nct product CTAs: the grid is one CTA per SM and fully co-resident
-  fence_acq_rel_gpu();
+  // barrier of the nct product CTAs: the grid is one CTA per SM and fully co-resident.  As in a
+  // cooperative grid sync, only thread 0 fences: bar.sync orders the CTA's forward-sum atomics before
+  // its gpu-scope release (cumulativity)
   __syncthreads();
   if (tid == 0) {
+    fence_acq_rel_gpu();
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(D.k1bar) : "memory");
     unsigned v;
     do {
@@ -612,9 +614,11 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
     unsigned long long ts2b;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts2b));
 #endif
-    fence_acq_rel_gpu();
     __syncthreads();
-    if (tid == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(D.fticket) : "memory");
+    if (tid == 0) {
+      fence_acq_rel_gpu();
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(D.fticket) : "memory");
+    }
 #if K1P_TIMING
     unsigned long long ts3;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts3));

@@ -88,15 +88,17 @@ __device__ void k2_finish(const Dev& D, const K2Ctx<RMAX>& C, K2Part<RMAX>& P, d
     if (D.update && m > 0.0)
       atomicMax(D.cmax + (size_t)((C.k + 1) & 1) * D.R + r, (unsigned long long)__double_as_longlong(m));
   }
-  fence_acq_rel_gpu();
+  // ticket as in a cooperative grid sync: bar.sync orders the CTA's partial stores before thread 0's
+  // gpu-scope fence and atomic (cumulativity); the last CTA's reads are ordered after its fence
   __syncthreads();
   if (tid == 0) {
+    fence_acq_rel_gpu();
     const unsigned t = atomicAdd(D.ticket, 1u);
     s_last = (t == gridDim.x - 1);
+    if (s_last) fence_acq_rel_gpu();
   }
   __syncthreads();
   if (!s_last) return;
-  fence_acq_rel_gpu();
 
   // ---------------- last CTA: R(w^k) for every active RHS (deterministic block sum over CTAs)
   __shared__ int s_rec[FSQR_MAXR];
