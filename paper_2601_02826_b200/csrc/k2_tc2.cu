@@ -619,8 +619,8 @@ __global__ void __launch_bounds__(Cfg2<16, 1>::THREADS, 1)
       if (c < D.p) {
         const int g0 = block_of_col(D, t * TILE_M + 1), g = block_of_col(D, c + 1);
         if (!PB.frozen[g]) {
-          const int sl = (g - g0) & 1;
-          const int32_t* Dk = dv + 4 * sl;
+          const bool sl = g != g0;   // second block of the tile: digit rows 4..7 (selects, not an indexed load)
+          const int32_t Dk[4] = {sl ? dv[4] : dv[0], sl ? dv[5] : dv[1], sl ? dv[6] : dv[2], sl ? dv[7] : dv[3]};
           PB.w[c + 1] = g_from_digits(D.n, D.colsum[c], PB.Tsum[g], PB.gs[g], D.inv_sd[c], Dk);
         }
       }
