@@ -38,6 +38,11 @@ void launch_lanczos_orth(const Dev& D, const double* v, const double* vp, double
 void launch_lanczos_next(const Dev& D, double* v, double* vp, const double* w, const double* beta, const int* frozen,
                          cudaStream_t st);
 void launch_null_score(const double* y, int n, const double* tau, int R, double* psi, cudaStream_t st);
+void launch_iota(int32_t* ix, int64_t p, cudaStream_t st);
+void launch_power_coef(const Dev& D, const double* v, const int* frozen, double* a, unsigned long long* cmax,
+                       cudaStream_t st);
+void launch_power_fwd_fin(const Dev& D, long long* sacc, long long* mterm, const unsigned long long* cmax, int maxcnt,
+                          const double* v, const int* frozen, double* u, double* Ug, cudaStream_t st);
 void launch_power_quant(const Dev& D, const double* u, const double* Ug, const int* frozen, int8_t* Bp, int ldk,
                         long long* Tsum, double* gs, double* w, cudaStream_t st);
 void launch_power_back_tc2(const Dev& D, const void* tmX, const void* tmBp, const long long* Tsum, const double* gs,
@@ -341,6 +346,53 @@ fsqr_status power_method(fsqr_ctx* ctx, cudaStream_t st) {
                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_err(ctx, FSQR_ERR_CUDA, "tensor map for the power digits failed (%d)", (int)r);
   }
+  // forward pass X~_g v_g on the tensor cores as well (k1_tcp in power mode: every column an entry,
+  // items spanning <= 2 blocks, one int64 accumulator row per block) when the forward product runs
+  // on k1_tcp for this storage
+  const bool tcfwd = tcback && D.k1_tc == 3;
+  Dev Dp = D;
+  double* acoef = nullptr;
+  if (tcfwd) {
+    int32_t* ident;
+    int *cntp, *stop0;
+    unsigned long long* cmx;
+    long long *sacc_pw, *mterm_pw;
+    AL(ident, (size_t)D.p);
+    AL(acoef, (size_t)D.p);
+    AL(cntp, 2);
+    AL(stop0, 1);
+    AL(cmx, 2);
+    AL(sacc_pw, (size_t)G * D.n);
+    AL(mterm_pw, G);
+    launch_iota(ident, D.p, st);
+    const int cnt2[2] = {(int)D.p, (int)D.p};
+    CK(cudaMemcpyAsync(cntp, cnt2, sizeof(cnt2), cudaMemcpyHostToDevice, st));
+    Dp.R = 1;
+    Dp.k1_pw = (int)D.gq + 1;
+    Dp.stop = stop0;
+    Dp.sup_cnt = cntp;
+    Dp.cmax = cmx;
+    Dp.sacc = sacc_pw;
+    Dp.mterm = mterm_pw;
+    for (int q = 0; q < 2; ++q) {
+      Dp.sup_idx[q] = ident;
+      Dp.sup_cs[q] = const_cast<int32_t*>(D.colsum);   // read only in k1_tcp
+      Dp.sup_c[q] = acoef;
+    }
+  }
+  auto fwd = [&](const double* vv, double* uu, double* ug) {
+    if (tcfwd) {
+      CK(cudaMemsetAsync(Dp.cmax, 0, 2 * sizeof(unsigned long long), st));
+      launch_power_coef(D, vv, d_frozen, acoef, Dp.cmax, st);
+      launch_k1_mode(Dp, ctx->k1_grid, st, 1);
+      launch_power_fwd_fin(D, Dp.sacc, Dp.mterm, Dp.cmax, Dp.k1_pw, vv, d_frozen, uu, ug, st);
+    } else if (geno) {
+      launch_power_fwd_int(D, d_bs, vv, d_frozen, part, S, uu, ug, st);
+    } else {
+      launch_power_fwd(D, d_bs, vv, d_frozen, uu, st);
+    }
+    return FSQR_OK;
+  };
   auto back = [&](const double* uu, const double* ug, double* ww) {
     if (tcback) {
       launch_power_quant(D, uu, ug, d_frozen, Bp, D.ldk, Tsum, gsc, ww, st);
@@ -369,7 +421,7 @@ fsqr_status power_method(fsqr_ctx* ctx, cudaStream_t st) {
     std::vector<double> h_alpha(G), h_beta(G);
     for (int it = 1; it <= ctx->opt.power_max_iter && live > 0; ++it) {
       if (geno) {
-        launch_power_fwd_int(D, d_bs, v, d_frozen, part, S, u, Ug, st);
+        fwd(v, u, Ug);
         back(u, Ug, w);
       } else {
         launch_power_fwd(D, d_bs, v, d_frozen, u, st);
@@ -405,7 +457,7 @@ fsqr_status power_method(fsqr_ctx* ctx, cudaStream_t st) {
   }
   for (int it = 1; it <= ctx->opt.power_max_iter && live > 0; ++it) {
     if (geno) {
-      launch_power_fwd_int(D, d_bs, v, d_frozen, part, S, u, Ug, st);
+      fwd(v, u, Ug);
       back(u, Ug, w);
     } else {
       launch_power_fwd(D, d_bs, v, d_frozen, u, st);

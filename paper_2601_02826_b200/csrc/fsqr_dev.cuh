@@ -38,6 +38,9 @@ struct Dev {
   int n, R, G, storage, npad, ldk;
   int k1_esmax;                     // k1_tcp: support entries per work item cap (<= 65536; FSQR_K1_ESMAX, tests)
   int k1_tc;                        // forward product: 0 k1_bulk (CUDA cores), 3 k1_tcp 2-bit, 4 k1_tcp u8 (tensor cores)
+  int k1_pw;                        // > 0: k1_tcp in power mode (a0' forward pass X~_g v_g for every block g): the
+                                    // entries are all columns, an item spans <= 2 blocks (slots 0/1 = blocks g0, g0+1),
+                                    // accumulator (and colsum term) of block g; the value is the max entries per block
   int x_policy;                     // L2 hint of the X stream in K2: 0 evict_first, 1 normal, 2 evict_last
   int k1_policy;                    // L2 hint of the forward gather: 0 evict_first, 1 normal, 2 evict_last
   int bperm;                        // 1: theta digit rows in the 2-bit tcgen05 K order (k2_tc2.cu)

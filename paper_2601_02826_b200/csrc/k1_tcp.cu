@@ -264,6 +264,9 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
   int64_t es = ((int64_t)max(cnt, 1) + per - 1) / per;
   // (u8 codes up to 255: 255 * 128 * 2^15 < 2^31, so at most 2^15 entries per item there)
   es = min((int64_t)min(D.k1_esmax, ST == 1 ? 32768 : 65536), ((es + KC - 1) / KC) * KC);
+  // power mode: an item must not span more than two blocks (the host guarantees >= 128 columns per block)
+  const bool pw = RMAX == 2 && D.k1_pw > 0;
+  if (pw) es = min(es, (int64_t)(D.gq - 1) / KC * KC);
   const int64_t nsl = ((int64_t)cnt + es - 1) / es;
   const int64_t nwork = (skip || reducer) ? 0 : nsl * nslab;
 
@@ -275,9 +278,9 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
     bool act[RMAX];
 #pragma unroll
     for (int r = 0; r < RMAX; ++r) {
-      act[r] = r < R && (cur || D.status[r] == ST_ACTIVE);
-      const double cm = r < R ? __longlong_as_double((long long)D.cmax[par * R + r]) : 0.0;
-      scale[r] = ldexp(1.0, fwd_exponent(cm, cnt, D.n));
+      act[r] = pw || (r < R && (cur || D.status[r] == ST_ACTIVE));
+      const double cm = (pw || r < R) ? __longlong_as_double((long long)D.cmax[pw ? par : par * R + r]) : 0.0;
+      scale[r] = ldexp(1.0, fwd_exponent(cm, pw ? (long long)D.k1_pw : (long long)cnt, D.n));
     }
     const uint64_t pol_m = policy_evict_normal();
     int bst = 0;
@@ -303,19 +306,30 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
       long long mt[RMAX];
 #pragma unroll
       for (int r = 0; r < RMAX; ++r) mt[r] = 0;
+      const int g0 = pw ? block_of_col(D, e0 + 1) : 0;   // power mode: the item's first block (entry e = column e)
       for (int64_t b = 0; b < nb; ++b) {
         const int buf = (int)((mbc + b) & 1);
         mbar_wait(&mfull[buf], (uint32_t)(((mbc + b) >> 1) & 1));
         const int64_t bs = e0 + b * MB, be = min(e1, bs + MB);
-        for (int64_t g0 = bs; g0 < be; g0 += KC) {
-          const bool live = g0 + lane < be;
-          const int o = (int)(g0 - bs) + lane;
+        for (int64_t g0e = bs; g0e < be; g0e += KC) {
+          const bool live = g0e + lane < be;
+          const int o = (int)(g0e - bs) + lane;
           const long long cs = (live && slab == 0) ? (long long)mcs[buf * MB + o] : 0;
           long long C[RMAX];
+          if (pw) {   // one coefficient per column, into the slot of its block
+            const long long cv = live ? __double2ll_rn(msc[buf * MB * RMAX + o] * scale[0]) : 0;
+            const int sl = live ? block_of_col(D, g0e + lane + 1) - g0 : 0;
 #pragma unroll
-          for (int r = 0; r < RMAX; ++r) {
-            C[r] = (live && act[r]) ? __double2ll_rn(msc[buf * MB * RMAX + o * R + r] * scale[r]) : 0;
-            mt[r] += cs * C[r];
+            for (int r = 0; r < RMAX; ++r) {
+              C[r] = sl == r ? cv : 0;
+              mt[r] += cs * C[r];
+            }
+          } else {
+#pragma unroll
+            for (int r = 0; r < RMAX; ++r) {
+              C[r] = (live && act[r]) ? __double2ll_rn(msc[buf * MB * RMAX + o * R + r] * scale[r]) : 0;
+              mt[r] += cs * C[r];
+            }
           }
           mbar_wait(&bempty[bst], bph ^ 1);
           uint8_t* bt = sB + bst * T::BTILE;
@@ -348,7 +362,7 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
           long long v = mt[r];
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-          if (lane == 0 && v != 0) atomicAdd((unsigned long long*)&D.mterm[r], (unsigned long long)v);
+          if (lane == 0 && v != 0) atomicAdd((unsigned long long*)&D.mterm[pw ? g0 + r : r], (unsigned long long)v);
         }
       }
     }
@@ -557,6 +571,8 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
       mbar_wait(tfull, tph);
       tph ^= 1;
       tc_fence_after();
+      const int gb = pw ? block_of_col(D, e0 + 1) : 0;                // power mode: accumulator of slot r is block gb + r
+      const int rlim = pw ? min(RMAX, D.G - gb) : R;
       const int m = q4 * 32 + lane;                                  // TMEM lane of the row tile
       const int qs = ST == 1 ? 0 : (m >> 2) & 3;                     // 2-bit plane: scale 4^qs
       const int rin = ST == 1 ? m : ((m & ~15) | ((m & 3) << 2) | qs);   // row within the tile
@@ -577,8 +593,8 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
           long long S = 0;
 #pragma unroll
           for (int q = 5; q >= 0; --q) S = S * 256 + (long long)dv[6 * r + q];
-          if (!(K1P_DBG & 8) && r < R && row < D.n && S != 0)
-            atomicAdd((unsigned long long*)&D.sacc[(int64_t)r * D.n + row], (unsigned long long)S);
+          if (!(K1P_DBG & 8) && r < rlim && row < D.n && S != 0)
+            atomicAdd((unsigned long long*)&D.sacc[(int64_t)(gb + r) * D.n + row], (unsigned long long)S);
         }
       }
       tc_fence_before();
@@ -689,7 +705,8 @@ void launch_r(const Dev& D, int grid, cudaStream_t st, int cur) {
 
 template <int ST>
 void launch_st(const Dev& D, int grid, cudaStream_t st, int cur) {
-  if (D.R <= 1) launch_r<1, ST>(D, grid, st, cur);
+  if (D.k1_pw > 0) launch_r<2, ST>(D, grid, st, cur);
+  else if (D.R <= 1) launch_r<1, ST>(D, grid, st, cur);
   else if (D.R <= 2) launch_r<2, ST>(D, grid, st, cur);
   else if (D.R <= 4) launch_r<4, ST>(D, grid, st, cur);
   else if (D.R <= 8) launch_r<8, ST>(D, grid, st, cur);

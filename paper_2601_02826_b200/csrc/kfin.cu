@@ -625,6 +625,59 @@ __global__ void __launch_bounds__(FT) k_power_quant(const Dev D, const double* u
   }
 }
 
+// ---- a0' forward pass on the tensor cores (k1_tcp power mode): coefficients, identity entry list,
+// and the per-block n-vectors from the exact int64 sums
+__global__ void k_iota(int32_t* ix, int64_t p) {
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < p; c += (int64_t)gridDim.x * blockDim.x)
+    ix[c] = (int32_t)c;
+}
+// a_c = v_{c+1} / s_c for every data column of a live block (0 in a frozen one); bits of max |a_c|
+// into both parity slots of cmax
+__global__ void k_power_coef(const Dev D, const double* v, const int* frozen, double* a, unsigned long long* cmax) {
+  unsigned long long m = 0;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < D.p; c += (int64_t)gridDim.x * blockDim.x) {
+    const double x = frozen[block_of_col(D, c + 1)] ? 0.0 : v[c + 1] * D.inv_sd[c];
+    a[c] = x;
+    const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(x));
+    m = b > m ? b : m;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long u = __shfl_xor_sync(0xffffffffu, m, o);
+    m = u > m ? u : m;
+  }
+  if ((threadIdx.x & 31) == 0 && m) {
+    atomicMax(cmax, m);
+    atomicMax(cmax + 1, m);
+  }
+}
+// per block g (one CTA each): u_gi = 2^-E (n S_gi - M_g) / n (+ v_0 for the intercept in block 0), the
+// same reconstruction as the finalize's s; Ug = sum_i u_gi (fixed order); then the accumulators are cleared
+__global__ void __launch_bounds__(FT) k_power_fwd_fin(const Dev D, long long* sacc, long long* mterm,
+                                                      const unsigned long long* cmax, int maxcnt, const double* v,
+                                                      const int* frozen, double* u, double* Ug) {
+  __shared__ double smd[33];
+  const int g = blockIdx.x;
+  if (frozen[g]) return;
+  const double inv = ldexp(1.0, -fwd_exponent(__longlong_as_double((long long)cmax[0]), maxcnt, D.n));
+  const long long M = mterm[g];
+  const double v0 = g == 0 ? v[0] : 0.0;
+  long long* sg = sacc + (int64_t)g * D.n;
+  double t = 0.0;
+  for (int i = threadIdx.x; i < D.n; i += blockDim.x) {
+    const double x = (double)((long long)D.n * sg[i] - M) * inv / (double)D.n + v0;
+    u[(int64_t)g * D.n + i] = x;
+    sg[i] = 0;
+    t += x;
+  }
+  double tt[1] = {t};
+  block_sum<1>(tt, smd);
+  if (threadIdx.x == 0) {
+    Ug[g] = tt[0];
+    mterm[g] = 0;
+  }
+}
+
 // per block g: est = v_g . w_g, nrm = ||w_g||  (one CTA per block, fixed order)
 __global__ void k_power_reduce(const int64_t* bstart, const double* v, const double* w, const int* frozen,
                                double* est, double* nrm) {
@@ -937,4 +990,13 @@ void launch_lla_weights(const Dev& D, int kind, double a, cudaStream_t st) {
 void launch_power_quant(const Dev& D, const double* u, const double* Ug, const int* frozen, int8_t* Bp, int ldk,
                         long long* Tsum, double* gs, double* w, cudaStream_t st) {
   k_power_quant<<<D.G, FT, 0, st>>>(D, u, Ug, frozen, Bp, ldk, Tsum, gs, w);
+}
+void launch_iota(int32_t* ix, int64_t p, cudaStream_t st) { k_iota<<<1184, 256, 0, st>>>(ix, p); }
+void launch_power_coef(const Dev& D, const double* v, const int* frozen, double* a, unsigned long long* cmax,
+                       cudaStream_t st) {
+  k_power_coef<<<1184, 256, 0, st>>>(D, v, frozen, a, cmax);
+}
+void launch_power_fwd_fin(const Dev& D, long long* sacc, long long* mterm, const unsigned long long* cmax, int maxcnt,
+                          const double* v, const int* frozen, double* u, double* Ug, cudaStream_t st) {
+  k_power_fwd_fin<<<D.G, FT, 0, st>>>(D, sacc, mterm, cmax, maxcnt, v, frozen, u, Ug);
 }
