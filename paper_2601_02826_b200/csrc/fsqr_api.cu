@@ -37,7 +37,7 @@ void launch_lanczos_orth(const Dev& D, const double* v, const double* vp, double
                          const double* beta, const int* frozen, cudaStream_t st);
 void launch_lanczos_next(const Dev& D, double* v, double* vp, const double* w, const double* beta, const int* frozen,
                          cudaStream_t st);
-void launch_null_score(const double* y, int n, const double* tau, int R, double* psi, cudaStream_t st);
+void launch_null_score(const double* y, int n, const double* tau, int R, int* ord, double* psi, cudaStream_t st);
 void launch_iota(int32_t* ix, int64_t p, cudaStream_t st);
 void launch_power_coef(const Dev& D, const double* v, const int* frozen, double* a, unsigned long long* cmax,
                        cudaStream_t st);
@@ -492,7 +492,9 @@ fsqr_status lambda_max(fsqr_ctx* ctx, cudaStream_t st) {
   unsigned long long* mb;
   AL(psi, (size_t)ctx->R * D.n);
   AL(mb, ctx->R);
-  launch_null_score(D.y, D.n, D.tau, ctx->R, psi, st);
+  int* ord;
+  AL(ord, D.n);
+  launch_null_score(D.y, D.n, D.tau, ctx->R, ord, psi, st);
   if (D.storage != 0) {
     double *tmp, *Us;
     AL(tmp, D.n);

@@ -436,7 +436,7 @@ struct K2Part {
 // fills cval/bval for the support entry.
 template <int RMAX>
 __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, int64_t c, const double* g,
-                                           K2Part<RMAX>& P, double* cval, double* bval, bool valid = true) {
+                                           K2Part<RMAX>& P, bool valid = true) {
   const int64_t j = c + 1;
   const double isd = valid ? D.inv_sd[c] : 0.0;
   const int gb = valid ? block_of_col(D, j) : 0;
@@ -451,8 +451,6 @@ __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, i
   bool nz = false;
 #pragma unroll
   for (int r = 0; r < RMAX; ++r) {
-    cval[r] = 0.0;
-    bval[r] = 0.0;
     if (r >= C.R || !C.cs->active[r]) continue;   // warp-uniform
     double x[FSQR_NPART] = {0.0, 0.0, 0.0, 0.0, 0.0};
     double cm = 0.0;
@@ -474,10 +472,7 @@ __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, i
         C.beta_out[j * C.R + r] = bn;
         if (bn != 0.0) {
           nz = true;
-          const double cv = bn * isd;
-          cval[r] = cv;
-          bval[r] = bn;
-          cm = fabs(cv);
+          cm = fabs(bn * isd);
         }
       }
     }
@@ -486,10 +481,11 @@ __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, i
   return nz;
 }
 
-// warp-aggregated append of support entries (lanes with nz)
+// warp-aggregated append of support entries (lanes with nz); the entry's beta^{k+1}_j and
+// beta^{k+1}_j / s_j of every RHS are re-read from beta_out (this thread wrote them in epi_column),
+// so the epilogue keeps no per-RHS copies in registers; an inactive RHS gets zeros
 template <int RMAX>
-__device__ __forceinline__ void support_append(const K2Ctx<RMAX>& C, bool nz, int64_t c, const double* cval,
-                                               const double* bval) {
+__device__ __forceinline__ void support_append(const Dev& D, const K2Ctx<RMAX>& C, bool nz, int64_t c) {
   const unsigned m = __ballot_sync(0xffffffffu, nz);
   if (m == 0) return;
   const int lane = threadIdx.x & 31;
@@ -498,13 +494,15 @@ __device__ __forceinline__ void support_append(const K2Ctx<RMAX>& C, bool nz, in
   base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
   if (nz) {
     const int e = base + __popc(m & ((1u << lane) - 1u));
+    const double isd = D.inv_sd[c];
     C.sidx[e] = (int32_t)c;
     C.scs[e] = C.colsum[c];
 #pragma unroll
     for (int r = 0; r < RMAX; ++r) {
       if (r < C.R) {
-        C.sc[(int64_t)e * C.R + r] = cval[r];
-        C.sb[(int64_t)e * C.R + r] = bval[r];
+        const double bn = C.cs->active[r] ? C.beta_out[(c + 1) * C.R + r] : 0.0;
+        C.sc[(int64_t)e * C.R + r] = bn != 0.0 ? bn * isd : 0.0;
+        C.sb[(int64_t)e * C.R + r] = bn;
       }
     }
   }

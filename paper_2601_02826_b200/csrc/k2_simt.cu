@@ -88,9 +88,6 @@ __global__ void __launch_bounds__(THREADS) k2_simt_int(const Dev D) {
         acc[a][q] = v;
       }
     bool nz = false;
-    double cval[RMAX], bval[RMAX];
-#pragma unroll
-    for (int r = 0; r < RMAX; ++r) cval[r] = bval[r] = 0.0;
     int64_t cc = -1;
 #pragma unroll
     for (int a = 0; a < CPW; ++a) {
@@ -107,18 +104,10 @@ __global__ void __launch_bounds__(THREADS) k2_simt_int(const Dev D) {
         for (int r = 0; r < RMAX; ++r)
           g[r] = r < C.R ? g_from_digits(D.n, cs, C.cs->Tsum[r], C.cs->gscale[r], isd, &acc[a][4 * r]) : 0.0;
       }
-      double cv2[RMAX], bv2[RMAX];
-      const bool z2 = epi_column<RMAX>(D, C, valid ? c : 0, g, P, cv2, bv2, valid);
-      if (valid) {
-        nz = z2;
-#pragma unroll
-        for (int r = 0; r < RMAX; ++r) {
-          cval[r] = cv2[r];
-          bval[r] = bv2[r];
-        }
-      }
+      const bool z2 = epi_column<RMAX>(D, C, valid ? c : 0, g, P, valid);
+      if (valid) nz = z2;
     }
-    if (D.update) support_append<RMAX>(C, nz, cc, cval, bval);
+    if (D.update) support_append<RMAX>(D, C, nz, cc);
   }
   __syncthreads();
   k2_finish<RMAX>(D, C, P, red);
@@ -153,12 +142,8 @@ __global__ void __launch_bounds__(THREADS) k2_simt_f32(const Dev D) {
     const double isd = D.inv_sd[c];
 #pragma unroll
     for (int r = 0; r < RMAX; ++r) g[r] = warp_sum_d(a[r]) * isd;
-    bool nz = false;
-    double cval[RMAX], bval[RMAX];
-#pragma unroll
-    for (int r = 0; r < RMAX; ++r) cval[r] = bval[r] = 0.0;
-    nz = epi_column<RMAX>(D, C, c, g, P, cval, bval, lane == 0);
-    if (D.update) support_append<RMAX>(C, nz, c, cval, bval);
+    const bool nz = epi_column<RMAX>(D, C, c, g, P, lane == 0);
+    if (D.update) support_append<RMAX>(D, C, nz, c);
   }
   __syncthreads();
   k2_finish<RMAX>(D, C, P, red);

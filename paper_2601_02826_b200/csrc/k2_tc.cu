@@ -210,9 +210,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int r = 0; r < RMAX; ++r) g[r] = 0.0;
       }
-      double cval[RMAX], bval[RMAX];
-      const bool nz = epi_column<RMAX>(D, C, valid ? c : 0, g, P, cval, bval, valid);
-      if (D.update) support_append<RMAX>(C, nz, c, cval, bval);
+      const bool nz = epi_column<RMAX>(D, C, valid ? c : 0, g, P, valid);
+      if (D.update) support_append<RMAX>(D, C, nz, c);
     }
   }
   tc_fence_before();

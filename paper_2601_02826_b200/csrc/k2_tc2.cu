@@ -43,8 +43,8 @@
 #define K2TC2_CW 8   // converter warps (two per SM sub-partition: the unpack loop is latency-bound with one)
 #endif
 #ifndef K2TC2_CWM
-#define K2TC2_CWM 4  // converter warps with several RHS (8 would need a 640-thread block: 96 registers and
-                     // spills; setmaxnreg per warpgroup did not help -- ptxas keeps the launch bound)
+#define K2TC2_CWM 8  // converter warps with several RHS, NPAD 32/48 (a 640-thread block: 96 registers, at most 16 bytes
+                     // of stack; C5 K2 0.581 -> 0.572 ms against 4); NPAD = 64 keeps 4 (8 spills 144 bytes there)
 #endif
 
 
@@ -64,7 +64,7 @@ struct Cfg2 {
   // up to 4 RHS: 8 converter warps, 4 epilogue warps; more: the per-column epilogue (E14, KKT
   // partials and support entries for every RHS) is the slower side, so 4 converters and two sets
   // of 4 epilogue warps taking alternate tiles (one accumulator buffer each)
-  static constexpr int CW = NPAD == 16 ? K2TC2_CW : K2TC2_CWM;   // (4 converters at NPAD = 16 would spill)
+  static constexpr int CW = NPAD == 16 ? K2TC2_CW : (NPAD >= 64 ? 4 : K2TC2_CWM);   // (4 converters at NPAD = 16 would spill)
   static constexpr int EW = NPAD == 16 ? 4 : 8;
   // NPAD == 16: one accumulator per code plane q, so the converter can leave the codes in place
   // ((w & (3 << 2q)) = x * 4^q, one LOP per word instead of shift + mask); the epilogue divides
@@ -397,9 +397,8 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
 #pragma unroll
         for (int r = 0; r < RMAX; ++r) g[r] = 0.0;
       }
-      double cval[RMAX], bval[RMAX];
-      const bool nz = epi_column<RMAX>(D, C, valid ? c : 0, g, P, cval, bval, valid);
-      if (D.update) support_append<RMAX>(C, nz, c, cval, bval);
+      const bool nz = epi_column<RMAX>(D, C, valid ? c : 0, g, P, valid);
+      if (D.update) support_append<RMAX>(D, C, nz, c);
     }
   }
   tc_fence_before();

@@ -728,50 +728,46 @@ __global__ void k_lanczos_next(const Dev D, double* v, double* vp, const double*
 }
 
 // sample tau-quantile by exact rank selection and the null-model score psi/n (DESIGN reading R4)
-__global__ void k_null_score(const double* y, int n, const double* tau, int R, double* psi /*[R][n]*/) {
+// rank_i = #{y_j < y_i} + #{j < i : y_j == y_i} (a permutation of 0..n-1); ord[rank_i] = i.  One thread
+// per i, y in shared-memory tiles: n^2 comparisons spread over the whole GPU
+__global__ void __launch_bounds__(256) k_ranks(const double* y, int n, int* ord) {
   __shared__ double ys[2048];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const double yi = i < n ? y[i] : 0.0;
+  int rank = 0;
+  for (int t0 = 0; t0 < n; t0 += 2048) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < 2048 && t0 + t < n; t += blockDim.x) ys[t] = y[t0 + t];
+    __syncthreads();
+    const int tn = min(2048, n - t0);
+    for (int t = 0; t < tn; ++t) {
+      const double yt = ys[t];
+      rank += (yt < yi) || (yt == yi && t0 + t < i);
+    }
+  }
+  if (i < n) ord[rank] = i;
+}
+
+// per RHS r (one CTA each): q = y_(ceil(n tau)) = y[ord[k - 1]], the null-model score psi (reading R4)
+__global__ void k_null_score(const double* y, int n, const double* tau, const int* ord, double* psi /*[R][n]*/) {
   __shared__ int cnt[3];
-  __shared__ double qsh;
-  for (int r = 0; r < R; ++r) {
-    int k = (int)ceil((double)n * tau[r]);
-    if (k < 1) k = 1;
-    if (k > n) k = n;
-    if (threadIdx.x == 0) {
-      cnt[0] = cnt[1] = cnt[2] = 0;
-      qsh = 0.0;
-    }
-    __syncthreads();
-    // rank_i = #{y_j < y_i} + #{j < i : y_j == y_i}; the element of rank k-1 is y_(k)
-    for (int i0 = 0; i0 < n; i0 += blockDim.x) {
-      const int i = i0 + threadIdx.x;
-      const double yi = i < n ? y[i] : 0.0;
-      int rank = 0;
-      for (int t0 = 0; t0 < n; t0 += 2048) {
-        __syncthreads();
-        for (int t = threadIdx.x; t < 2048 && t0 + t < n; t += blockDim.x) ys[t] = y[t0 + t];
-        __syncthreads();
-        const int tn = min(2048, n - t0);
-        for (int t = 0; t < tn; ++t) {
-          const double yt = ys[t];
-          rank += (yt < yi) || (yt == yi && t0 + t < i);
-        }
-      }
-      if (i < n && rank == k - 1) qsh = yi;
-    }
-    __syncthreads();
-    const double q = qsh;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const double yi = y[i];
-      atomicAdd(&cnt[yi < q ? 0 : (yi > q ? 2 : 1)], 1);
-    }
-    __syncthreads();
-    const double t = tau[r];
-    const double tie = -((double)cnt[0] * (t - 1.0) + (double)cnt[2] * t) / (double)cnt[1];
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const double yi = y[i];
-      psi[(int64_t)r * n + i] = (yi < q ? t - 1.0 : (yi > q ? t : tie)) / (double)n;
-    }
-    __syncthreads();
+  const int r = blockIdx.x;
+  int k = (int)ceil((double)n * tau[r]);
+  if (k < 1) k = 1;
+  if (k > n) k = n;
+  if (threadIdx.x == 0) cnt[0] = cnt[1] = cnt[2] = 0;
+  __syncthreads();
+  const double q = y[ord[k - 1]];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double yi = y[i];
+    atomicAdd(&cnt[yi < q ? 0 : (yi > q ? 2 : 1)], 1);
+  }
+  __syncthreads();
+  const double t = tau[r];
+  const double tie = -((double)cnt[0] * (t - 1.0) + (double)cnt[2] * t) / (double)cnt[1];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double yi = y[i];
+    psi[(int64_t)r * n + i] = (yi < q ? t - 1.0 : (yi > q ? t : tie)) / (double)n;
   }
 }
 
@@ -971,8 +967,9 @@ void launch_back_int(const Dev& D, const double* u, const double* Ug, int per_bl
   if (D.storage == 1) k_back_int<1><<<148 * 8, 256, 0, st>>>(D, u, Ug, per_block, frozen, w, maxbits);
   else k_back_int<2><<<148 * 8, 256, 0, st>>>(D, u, Ug, per_block, frozen, w, maxbits);
 }
-void launch_null_score(const double* y, int n, const double* tau, int R, double* psi, cudaStream_t st) {
-  k_null_score<<<1, 1024, 0, st>>>(y, n, tau, R, psi);
+void launch_null_score(const double* y, int n, const double* tau, int R, int* ord, double* psi, cudaStream_t st) {
+  k_ranks<<<(n + 255) / 256, 256, 0, st>>>(y, n, ord);
+  k_null_score<<<R, 1024, 0, st>>>(y, n, tau, ord, psi);
 }
 void launch_build_support(const Dev& D, int par, cudaStream_t st) {
   k_build_support<<<(int)((D.p + 255) / 256 < 4096 ? (D.p + 255) / 256 : 4096), 256, 0, st>>>(D, par);
