@@ -323,10 +323,35 @@ __global__ void k_colstats_int(const Dev D, int32_t* colsum, double* mean, doubl
   for (int64_t c = gw; c < D.p; c += nw) {
     const uint8_t* col = D.X8 + c * D.ld;
     long long s1 = 0, s2 = 0;
-    for (int i = lane; i < D.n; i += 32) {
-      const int g = ST == 1 ? col[i] : (col[i >> 2] >> (2 * (i & 3))) & 3;
-      s1 += g;
-      s2 += g * g;
+    // 16-byte loads over the stored bytes of the column (the padding past n is zero, so it adds 0):
+    // u8 sums by dp4a (sum of bytes, sum of squares); 2-bit codes c = b0 + 2 b1 by popcounts:
+    // sum c = |b0| + 2|b1|, sum c^2 = |b0| + 4|b1| + 4|b0 b1|
+    const int nb = (int)min(D.ld, (int64_t)(ST == 1 ? (D.n + 15) / 16 * 16 : ((D.n + 3) / 4 + 15) / 16 * 16));
+    for (int off = lane * 16; off < nb; off += 512) {
+      const uint4 v = __ldcs((const uint4*)(col + off));
+      uint32_t w[4] = {v.x, v.y, v.z, v.w};
+      // samples past n in the last chunk are masked (the layout's padding is zero, but do not rely on it)
+      const int valid = ST == 1 ? D.n - off : D.n - 4 * off;   // samples of this chunk that exist
+      if (valid < (ST == 1 ? 16 : 64)) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int k = valid - (ST == 1 ? 4 : 16) * q;   // samples of word q that exist
+          const int bits = k <= 0 ? 0 : (ST == 1 ? 8 * k : 2 * k);
+          if (bits < 32) w[q] &= bits == 0 ? 0u : (0xFFFFFFFFu >> (32 - bits));
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (ST == 1) {
+          s1 += (unsigned)__dp4a(w[q], 0x01010101u, 0u);
+          s2 += (unsigned)__dp4a(w[q], w[q], 0u);
+        } else {
+          const uint32_t lo = w[q] & 0x55555555u, hi = w[q] & 0xAAAAAAAAu;
+          const int a = __popc(lo), b = __popc(hi), ab = __popc(lo & (hi >> 1));
+          s1 += a + 2 * b;
+          s2 += a + 4 * b + 4 * ab;
+        }
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

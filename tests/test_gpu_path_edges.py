@@ -184,3 +184,21 @@ def test_unpenalised_full_support(cuda_ok, storage):
     assert o["status"] == 0
     assert np.count_nonzero(S.beta()[0][1:]) == prob.p
     assert S.objective()[0] == pytest.approx(o["obj"], rel=1e-6)
+
+
+@pytest.mark.parametrize("taus", [[0.5], [0.1, 0.25, 0.9]])
+def test_lambda_max_with_tied_responses(cuda_ok, taus):
+    """lambda_max (reading R4) when y has many ties, including at the quantile itself: the GPU ranks
+    y over the whole grid (k_ranks, ties broken by index) and gives the tie group the score that makes
+    sum(psi) = 0; it must equal the oracle's lambda_max and quantile, every tau, to 1e-10."""
+    import paper_2601_02826_b200 as fs
+
+    prob = datagen.make("c2", n=1500, p=800)
+    prob.y = np.round(prob.y, 1)          # ~130 distinct values over 1500 observations
+    d = oracle.Design.from_problem(prob)
+    X, y = to_device(prob)
+    S = fs.Solver(X, prob.storage, prob.n, prob.p, prob.ld, y, taus, [1.0] * len(taus), G=prob.G)
+    lm = S.lambda_max()
+    for r, t in enumerate(taus):
+        lo, q = oracle.lambda_max(d, prob.y, t)
+        assert lm[r] == pytest.approx(lo, rel=1e-10, abs=1e-15), (t, lm[r], lo)
