@@ -54,6 +54,9 @@ __device__ __forceinline__ unsigned __smid() {
 #ifndef K1P_CTAS
 #define K1P_CTAS 1     // CTAs per SM the launch grid assumes
 #endif
+#ifndef K1P_L2PF
+#define K1P_L2PF 0     // L2 prefetch of the next X~^T theta pass's first tiles (measurement knob)
+#endif
 #ifndef K1P_TIMING
 #define K1P_TIMING 0   // measurement build: per-CTA globaltimer stamps of iteration K1P_TIMING (fsqr_debug_stamps)
 #endif
@@ -241,6 +244,21 @@ __global__ void __launch_bounds__(THREADS, K1P_CTAS) k1_tcp_kernel(const Dev D, 
   const uint32_t tmem_base = *tmem_slot;
   pdl_launch_dependents();
   pdl_wait();
+#if K1P_L2PF
+  // 2-bit, iteration mode: pull the first column tile the next X~^T theta pass will stream on this
+  // CTA's index (128 columns, contiguous) into L2 while this kernel runs -- HBM is nearly idle here
+  if (ST == 2 && !cur && threadIdx.x == 0 && D.k1_pw == 0) {
+    const int64_t c0 = (int64_t)blockIdx.x * 128;
+    if (c0 < D.p) {
+      const int64_t bytes = (min((int64_t)D.p, c0 + 128) - c0) * D.ld;
+      const uint8_t* base = D.X8 + c0 * D.ld;
+      for (int64_t o = 0; o < bytes; o += 32768) {
+        const uint32_t sz = (uint32_t)min((int64_t)32768, bytes - o);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + o), "r"(sz) : "memory");
+      }
+    }
+  }
+#endif
 #if K1P_TIMING
   unsigned long long ts0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts0));
