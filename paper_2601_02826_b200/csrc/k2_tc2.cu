@@ -39,6 +39,14 @@
 #ifndef K2TC2_L2PF
 #define K2TC2_L2PF 0    // k-blocks of the next pass's first tiles prefetched into L2 at the end of a pass (measured: 20 or 40 cost 2-3% at M, so off)
 #endif
+#ifndef K2TC2_PARK
+#define K2TC2_PARK 0   // 1: every pipeline wait of k2_tc2_kernel parks the warp (try_wait suspend hint)
+#endif
+#if K2TC2_PARK
+#define K2_WAIT mbar_wait_park
+#else
+#define K2_WAIT mbar_wait
+#endif
 #ifndef K2TC2_CW
 #define K2TC2_CW 8   // converter warps (two per SM sub-partition: the unpack loop is latency-bound with one)
 #endif
@@ -214,7 +222,7 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
       uint32_t phase = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          K2_WAIT(&empty[stage], phase ^ 1);
           if (elect_one()) {
             mbar_expect_tx(&full[stage], bytes);
             tma_load_2d(sA + stage * A_BYTES, &tmX, &full[stage], kb * PK, (int)(t * TILE_M), pol_x);
@@ -254,12 +262,12 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
         const int acc = lt & 1;
         const uint32_t tph = (lt >> 1) & 1;
-        mbar_wait(&tempty[acc], tph ^ 1);
+        K2_WAIT(&tempty[acc], tph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tbase + (uint32_t)(acc * CF::ACC_COLS);
         for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(&full[stage], phase);
-          mbar_wait(&afull[ab], aphase);
+          K2_WAIT(&full[stage], phase);
+          K2_WAIT(&afull[ab], aphase);
           tc_fence_after();
           const uint32_t a_tmem = tbase + (uint32_t)(A_COL0 + ab * A_COLS);
           const uint64_t bdesc0 = umma_desc_sw128(sB0 + (uint32_t)(stage * CF::B_BYTES));
@@ -302,8 +310,8 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
     uint32_t phase = 0, aphase = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       for (int kb = 0; kb < kblocks; ++kb) {
-        mbar_wait(&full[stage], phase);
-        mbar_wait(&aempty[ab], aphase ^ 1);
+        K2_WAIT(&full[stage], phase);
+        K2_WAIT(&aempty[ab], aphase ^ 1);
         tc_fence_after();
         uint32_t w[NW], w4[CF::SPLITQ ? 1 : NW];
         const uint8_t* row = sA + stage * A_BYTES + c * PK;
