@@ -81,7 +81,8 @@ enum {
   /* U8 storage only: at create, repack the codes into an OWNED 2-bit copy (fsqr_pack2) and run the
    * PACKED2 kernels on it, so every iteration streams n*p/4 instead of n*p bytes (DESIGN.md §5,
    * "storage").  Codes must be in {0..3} (else FSQR_ERR_DATA); data_dev is read only during
-   * create and may be freed afterwards.  Results are those of PACKED2 storage on the same codes. */
+   * create and may be freed afterwards.  Results are those of PACKED2 storage on the same codes.
+   * The owned copy's column stride is ceil(n/4) rounded up to 128 bytes (aligned TMA rows). */
   FSQR_DESIGN_PACK2 = 1
 };
 
