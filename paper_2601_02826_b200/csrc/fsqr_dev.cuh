@@ -248,6 +248,18 @@ __device__ __forceinline__ void mbar_wait_park(uint64_t* b, uint32_t parity) {
       "r"(parity), "r"(0x100000u)
       : "memory");
 }
+// one non-blocking probe of a phase (for waits that back off with __nanosleep)
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, uint64_t* bar, int x, int y,
                                             uint64_t policy) {
   asm volatile(
@@ -434,9 +446,12 @@ struct K2Part {
 // Writes beta^{k+1}, accumulates R_beta(w^k) partials and the penalty of beta^k,
 // returns whether beta^{k+1}_j != 0 for some active RHS (support membership) and
 // fills cval/bval for the support entry.
+// bsrc / bdst: this column's R values of beta^k / beta^{k+1} ([j][R] rows of the state, or a
+// shared-memory staging copy of them; nullptr = the state rows C.beta_in / C.beta_out + j R)
 template <int RMAX>
 __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, int64_t c, const double* g,
-                                           K2Part<RMAX>& P, bool valid = true) {
+                                           K2Part<RMAX>& P, bool valid = true, const double* bsrc = nullptr,
+                                           double* bdst = nullptr) {
   const int64_t j = c + 1;
   const double isd = valid ? D.inv_sd[c] : 0.0;
   const int gb = valid ? block_of_col(D, j) : 0;
@@ -447,7 +462,10 @@ __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, i
   // hoisting the next RHS's global load over them (one memory latency per RHS per column)
   double bin[RMAX];
 #pragma unroll
-  for (int r = 0; r < RMAX; ++r) bin[r] = (valid && r < C.R) ? C.beta_in[j * C.R + r] : 0.0;
+  if (!bsrc) bsrc = C.beta_in + j * C.R;
+  if (!bdst) bdst = C.beta_out + j * C.R;
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) bin[r] = (valid && r < C.R) ? bsrc[r] : 0.0;
   bool nz = false;
 #pragma unroll
   for (int r = 0; r < RMAX; ++r) {
@@ -469,7 +487,7 @@ __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, i
         // E14, or the elastic-net block prox (Remark 3, L347-349; reading R19) when lam2 > 0
         const double bn = l2 == 0.0 ? prox_beta_inv(b, g[r], lam, eta, inv_eta)
                                     : (pos_part(eta * b + g[r] - lam) - pos_part(-eta * b - g[r] - lam)) / (eta + l2);
-        C.beta_out[j * C.R + r] = bn;
+        bdst[r] = bn;
         if (bn != 0.0) {
           nz = true;
           cm = fabs(bn * isd);
@@ -485,7 +503,8 @@ __device__ __forceinline__ bool epi_column(const Dev& D, const K2Ctx<RMAX>& C, i
 // beta^{k+1}_j / s_j of every RHS are re-read from beta_out (this thread wrote them in epi_column),
 // so the epilogue keeps no per-RHS copies in registers; an inactive RHS gets zeros
 template <int RMAX>
-__device__ __forceinline__ void support_append(const Dev& D, const K2Ctx<RMAX>& C, bool nz, int64_t c) {
+__device__ __forceinline__ void support_append(const Dev& D, const K2Ctx<RMAX>& C, bool nz, int64_t c,
+                                               const double* bout = nullptr) {
   const unsigned m = __ballot_sync(0xffffffffu, nz);
   if (m == 0) return;
   const int lane = threadIdx.x & 31;
@@ -500,7 +519,7 @@ __device__ __forceinline__ void support_append(const Dev& D, const K2Ctx<RMAX>& 
 #pragma unroll
     for (int r = 0; r < RMAX; ++r) {
       if (r < C.R) {
-        const double bn = C.cs->active[r] ? C.beta_out[(c + 1) * C.R + r] : 0.0;
+        const double bn = C.cs->active[r] ? (bout ? bout[r] : C.beta_out[(c + 1) * C.R + r]) : 0.0;
         C.sc[(int64_t)e * C.R + r] = bn != 0.0 ? bn * isd : 0.0;
         C.sb[(int64_t)e * C.R + r] = bn;
       }
@@ -514,11 +533,13 @@ __device__ __forceinline__ void prefetch_l1(const void* p) {
 // L1 prefetch of the per-column state the a2 epilogue reads for data column c (beta^k of every RHS,
 // colsum, 1/s_j), issued one tile ahead: the epilogue's loads then hit L1 instead of waiting on HBM
 template <int RMAX>
-__device__ __forceinline__ void epi_prefetch(const Dev& D, const K2Ctx<RMAX>& C, int64_t c) {
+__device__ __forceinline__ void epi_prefetch(const Dev& D, const K2Ctx<RMAX>& C, int64_t c, bool beta = true) {
   if (c >= D.p) return;
-  const double* b = C.beta_in + (c + 1) * C.R;
-  prefetch_l1(b);
-  if (C.R > 1) prefetch_l1(b + C.R - 1);
+  if (beta) {
+    const double* b = C.beta_in + (c + 1) * C.R;
+    prefetch_l1(b);
+    if (C.R > 1) prefetch_l1(b + C.R - 1);
+  }
   prefetch_l1(D.colsum + c);
   prefetch_l1(D.inv_sd + c);
 }

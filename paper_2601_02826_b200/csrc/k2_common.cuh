@@ -45,19 +45,22 @@ __device__ void k2_load_ctx(const Dev& D, K2Ctx<RMAX>& C) {
 // every thread of the block; `red` needs blockDim/32 * RMAX * (NPART+1) doubles.
 // zero the reduction buffer and point a shared-memory-mode K2Part at this warp's slot (all threads,
 // before k2_load_ctx, whose block barrier orders the zeroing before any epilogue add)
+// In shared-memory mode a kernel whose partials come from a subset of its warps may pass that
+// warp's slot and the number of slots (red then needs only nslots * RMAX * (NPART+1) doubles).
 template <int RMAX>
-__device__ __forceinline__ void k2_part_init(K2Part<RMAX>& P, double* red) {
+__device__ __forceinline__ void k2_part_init(K2Part<RMAX>& P, double* red, int slot = -1, int nslots = -1) {
   P.zero();
   if constexpr (K2Part<RMAX>::SM) {
-    const int nw = blockDim.x >> 5;
+    const int nw = nslots < 0 ? (int)(blockDim.x >> 5) : nslots;
     for (int q = threadIdx.x; q < nw * RMAX * (FSQR_NPART + 1); q += blockDim.x) red[q] = 0.0;
-    P.slot = red + (threadIdx.x >> 5) * RMAX * (FSQR_NPART + 1);
+    P.slot = red + (slot < 0 ? (int)(threadIdx.x >> 5) : slot) * RMAX * (FSQR_NPART + 1);
   }
 }
 
 template <int RMAX>
-__device__ void k2_finish(const Dev& D, const K2Ctx<RMAX>& C, K2Part<RMAX>& P, double* red) {
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+__device__ void k2_finish(const Dev& D, const K2Ctx<RMAX>& C, K2Part<RMAX>& P, double* red, int nslots = -1) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nw = (K2Part<RMAX>::SM && nslots >= 0) ? nslots : (int)(blockDim.x >> 5);
   constexpr int W = FSQR_NPART + 1;
   if constexpr (!K2Part<RMAX>::SM) {   // shared-memory mode: the per-warp slots are already in red
 #pragma unroll

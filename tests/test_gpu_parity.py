@@ -144,9 +144,14 @@ def test_multi_rhs_matches_single(cuda_ok):
         S = fs.Solver(X, 1, prob.n, prob.p, prob.ld, y, [t], [l], G=5, eta=eta)
         S.iterate(40)
         b, z, th = S.state()
-        # not bitwise: the int64 fixed-point scale of a4 depends on the union support size
+        # not bitwise: the fixed-point exponent of the a4 forward product (k1_fwd.cu, 2^E beta/s in
+        # 48 bits) is chosen from the largest |beta_j/s_j| over the RHS that share the launch, so a
+        # lockstep RHS is quantised on a coarser grid than its single solve (relative 2^-47 of that
+        # max per coefficient).  Norm-wise and element by element (scaled by the vector's max):
         assert rel(bm[r], b[0]) < 1e-9
         assert rel(tm[r], th[0]) < 1e-9
+        assert np.max(np.abs(bm[r] - b[0])) <= 1e-9 * np.max(np.abs(b[0]))
+        assert np.max(np.abs(tm[r] - th[0])) <= 1e-9 * np.max(np.abs(th[0]))
         assert np.array_equal(bm[r] != 0, b[0] != 0)
 
 
