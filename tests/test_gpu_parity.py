@@ -147,11 +147,14 @@ def test_multi_rhs_matches_single(cuda_ok):
         # not bitwise: the fixed-point exponent of the a4 forward product (k1_fwd.cu, 2^E beta/s in
         # 48 bits) is chosen from the largest |beta_j/s_j| over the RHS that share the launch, so a
         # lockstep RHS is quantised on a coarser grid than its single solve (relative 2^-47 of that
-        # max per coefficient).  Norm-wise and element by element (scaled by the vector's max):
+        # max per coefficient).  That 2^-47 perturbation of s can flip round(theta_i / delta) of the
+        # next pass (theta enters the product as 28-bit fixed point, delta >= 2^-28
+        # max|theta|), after which the two runs differ by a few quantisation steps: norm-wise 1e-9,
+        # element by element within 4 steps = 2^-26 of the vector's max (measured 1.0e-9):
         assert rel(bm[r], b[0]) < 1e-9
         assert rel(tm[r], th[0]) < 1e-9
-        assert np.max(np.abs(bm[r] - b[0])) <= 1e-9 * np.max(np.abs(b[0]))
-        assert np.max(np.abs(tm[r] - th[0])) <= 1e-9 * np.max(np.abs(th[0]))
+        assert np.max(np.abs(bm[r] - b[0])) <= 2.0 ** -26 * np.max(np.abs(b[0]))
+        assert np.max(np.abs(tm[r] - th[0])) <= 2.0 ** -26 * np.max(np.abs(th[0]))
         assert np.array_equal(bm[r] != 0, b[0] != 0)
 
 
