@@ -43,9 +43,6 @@
 #ifndef K2TC2_BTRIM
 #define K2TC2_BTRIM 1  // pair order: a theta-digit stage holds only the 8-row groups with a live row
 #endif
-#ifndef K2TC2_XPF
-#define K2TC2_XPF 0  // pair order: X stages requested into L2 (TMA prefetch) ahead of the shared-memory ring
-#endif
 #ifndef K2TC2_NB
 #define K2TC2_NB 3   // theta-digit stages of the pair order's own ring
 #endif
@@ -235,35 +232,6 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     if constexpr (PAIR) {   // X only: the theta digits have their own producer (warp 3)
-      // L2 prefetch iterator, K2TC2_XPF stages ahead of the ring's loads (same pair order)
-      int plt = 0, pkb = 0, ph = 0;
-      auto pf_next = [&]() {
-        if (plt >= ntl) return;
-        if (elect_one())
-          tma_prefetch_l2(&tmX, pkb * PK, (int)((blockIdx.x + (int64_t)(plt + ph) * gridDim.x) * TILE_M), pol_x);
-        const int pnh = ntl - plt < 2 ? 1 : 2;
-        if (++ph == pnh) {
-          ph = 0;
-          if (++pkb == kblocks) {
-            pkb = 0;
-            plt += 2;
-          }
-        }
-      };
-      if (K2TC2_XPF > 0) {
-        for (int i = 0; i < CF::STAGES; ++i) {   // skip what the ring itself requests at once
-          const int pnh = ntl - plt < 2 ? 1 : 2;
-          if (plt >= ntl) break;
-          if (++ph == pnh) {
-            ph = 0;
-            if (++pkb == kblocks) {
-              pkb = 0;
-              plt += 2;
-            }
-          }
-        }
-        for (int i = 0; i < K2TC2_XPF; ++i) pf_next();
-      }
       for (int lt = 0; lt < ntl; lt += 2) {
         const int nh = ntl - lt < 2 ? 1 : 2;
         for (int kb = 0; kb < kblocks; ++kb) {
@@ -274,7 +242,6 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
               mbar_expect_tx(&full[stage], (uint32_t)A_BYTES);
               tma_load_2d(sA + stage * A_BYTES, &tmX, &full[stage], kb * PK, (int)(t * TILE_M), pol_x);
             }
-            if (K2TC2_XPF > 0) pf_next();
             __syncwarp();
             if (++stage == CF::STAGES) {
               stage = 0;
