@@ -239,11 +239,14 @@ def test_k1_tcp_many_work_items_per_cta(cuda_ok, monkeypatch, esmax, taus):
         np.testing.assert_array_equal(u, v)
 
 
-@pytest.mark.parametrize("taus", [[0.5], [0.25, 0.5, 0.75], [k / 10 for k in range(1, 10)], [k / 17 for k in range(1, 17)]])
+@pytest.mark.parametrize("taus", [[0.5], [0.25, 0.5, 0.75], [k / 6 for k in range(1, 6)], [k / 10 for k in range(1, 10)],
+                                  [k / 17 for k in range(1, 17)]])
 def test_tc2_several_tiles_per_cta_equals_simt(cuda_ok, taus):
     """p = 40,000 columns = 313 tiles of 128 over at most 148 persistent CTAs, so every CTA of the
     2-bit tensor-core kernel carries its TMA ring, A buffers and double-buffered accumulators
-    across tiles; the exact-integer dp4a kernel gives the same state bit for bit."""
+    across tiles (two or three tiles per CTA: with 5, 9 and 16 RHS the tile-pair order runs a full
+    pair and, on the CTAs with three tiles, a single-tile tail); the exact-integer dp4a kernel gives
+    the same state bit for bit."""
     import paper_2601_02826_b200 as fs
 
     b = datagen.make("c5", n=700, p=40000, storage=fs.PACKED2)
