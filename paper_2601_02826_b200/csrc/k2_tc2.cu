@@ -30,52 +30,8 @@
 #ifndef K2TC2_SMEM_KB
 #define K2TC2_SMEM_KB 226
 #endif
-#ifndef K2TC2_NOMMA
-#define K2TC2_NOMMA 0   // measurement variant: skip the MMAs (wrong results)
-#endif
-#ifndef K2TC2_BATOMS
-#define K2TC2_BATOMS 4   // theta-digit atoms loaded per stage (4; fewer only in measurement variants)
-#endif
-#ifndef K2TC2_L2PF
-#define K2TC2_L2PF 0    // k-blocks of the next pass's first tiles prefetched into L2 at the end of a pass (measured: 20 or 40 cost 2-3% at M, so off)
-#endif
-#ifndef K2TC2_PARK
-#define K2TC2_PARK 0   // 1: every pipeline wait of k2_tc2_kernel parks the warp (try_wait suspend hint)
-#endif
-#if K2TC2_PARK
-#define K2_WAIT mbar_wait_park
-#else
-#define K2_WAIT mbar_wait
-#endif
 #ifndef K2TC2_CW
 #define K2TC2_CW 8   // converter warps (two per SM sub-partition: the unpack loop is latency-bound with one)
-#endif
-#ifndef K2TC2_NOCONV
-#define K2TC2_NOCONV 0  // measurement variant: converters skip the unpack (wrong results)
-#endif
-#ifndef K2TC2_NOEPI
-#define K2TC2_NOEPI 0   // measurement variant: epilogue skips the per-column work (wrong results)
-#endif
-#ifndef K2TC2_ACC1
-#define K2TC2_ACC1 0    // several RHS: one accumulator buffer (the MMA of tile t waits for the epilogue's TMEM
-                        // read of tile t-1), so a third TMEM A buffer fits at NPAD = 48
-#endif
-#ifndef K2TC2_BSTG
-#define K2TC2_BSTG 0    // 5+ RHS: the epilogue stages each tile's beta^k / beta^{k+1} rows ([j][R], 8R bytes per
-                        // column) through shared memory -- cp.async prefetch one set-tile ahead, coalesced
-                        // write-back -- instead of R strided 8-byte loads and stores per column
-#endif
-#ifndef K2TC2_ESLEEP
-#define K2TC2_ESLEEP 0  // > 0: the epilogue waits for its accumulator with test_wait + __nanosleep(ns) instead of
-                        // a try_wait spin (the spin took issue slots from the converter warps)
-#endif
-#ifndef K2TC2_ALT
-#define K2TC2_ALT 0     // 1: the two converter warps of a TMEM lane quarter take alternate stages (whole rows)
-                        // instead of the two halves of every stage: two stages in conversion at once
-#endif
-#ifndef K2TC2_SQ48
-#define K2TC2_SQ48 0    // 1: NPAD = 48 (C5's nine RHS) also keeps one accumulator per code plane (codes in place, four
-                        // LOPs per packed word instead of five), with a single accumulator buffer to fit TMEM
 #endif
 #ifndef K2TC2_CWM
 #define K2TC2_CWM 8  // converter warps with several RHS, NPAD 32/48 (a 640-thread block: 96 registers, at most 16 bytes
@@ -110,7 +66,6 @@ struct Cfg2 {
   // partials and support entries for every RHS) is the slower side, so 4 converters and two sets
   // of 4 epilogue warps taking alternate tiles (one accumulator buffer each)
   static constexpr int CW = NPAD == 16 ? K2TC2_CW : (NPAD >= 64 ? 4 : K2TC2_CWM);   // (4 converters at NPAD = 16 would spill)
-  static constexpr bool ALT = K2TC2_ALT && CW == 8;   // converter warps h = 0/1 take alternate stages
   static constexpr int EW = NPAD == 16 ? 4 : 8;
   // NPAD == 16: one accumulator per code plane q, so the converter can leave the codes in place
   // ((w & (3 << 2q)) = x * 4^q, one LOP per word instead of shift + mask); the epilogue divides
@@ -118,10 +73,9 @@ struct Cfg2 {
   // NPAD > 16 (several RHS): four planes would not fit next to the A buffers, so two scale
   // groups: with w4 = w >> 4 (one SHF per word), planes 0 and 2 are w & M and w4 & M (x 1),
   // planes 1 and 3 are w & (M << 2) and w4 & (M << 2) (x 4): 5 instructions per word instead of 8.
-  static constexpr bool SPLITQ = NPAD == 16 || (K2TC2_SQ48 && NPAD == 48);
+  static constexpr bool SPLITQ = NPAD == 16;
   static constexpr int ACC_COLS = SPLITQ ? 4 * NPAD : 2 * NPAD;   // columns of one accumulator buffer
-  static constexpr bool ACC1 = SPLITQ ? NPAD > 16 : K2TC2_ACC1 != 0;   // (4 planes x 48 columns: one buffer)
-  static constexpr int A_COL0 = (ACC1 ? 1 : 2) * ACC_COLS;        // A buffers after the accumulator(s)
+  static constexpr int A_COL0 = 2 * ACC_COLS;                     // A buffers after the accumulators
   static constexpr int NAB = (512 - A_COL0) / A_COLS < 3 ? (512 - A_COL0) / A_COLS : 3;   // TMEM A buffers
   static_assert(NAB >= 2, "TMEM budget");
   static constexpr int THREADS = 32 * (4 + CW + EW);
@@ -129,17 +83,12 @@ struct Cfg2 {
   static constexpr int B_BYTES = 4 * B_ATOM;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int RMAX = RM;   // RHS slots compiled in (<= NPAD / 4)
-  static constexpr bool BSTG = K2TC2_BSTG && K2Part<RMAX>::SM;   // staged beta (shared-memory partials mode)
-  static constexpr int ESETS = EW / 4;
-  // partial-sum slots: every warp, or (staged mode) the epilogue warps only
-  static constexpr int NSLOT = BSTG ? EW : THREADS / 32;
-  static constexpr int RED0 = NSLOT * RMAX * (FSQR_NPART + 1);
+  static constexpr int RED0 = (THREADS / 32) * RMAX * (FSQR_NPART + 1);
   static constexpr int RED_DOUBLES = RED0 > 33 * FSQR_NPART ? RED0 : 33 * FSQR_NPART;
-  static constexpr int BST_DOUBLES = BSTG ? ESETS * TILE_M * RMAX : 0;   // one beta tile per epilogue set
   // as many stages as fit: several RHS make the theta-digit B tile (4 x NPAD x 128 B) larger than
   // the 16 KB X tile, and the X bytes in flight are what keep HBM busy
-  static constexpr int STAGES = (K2TC2_SMEM_KB * 1024 - 2048 - RED_DOUBLES * 8 - BST_DOUBLES * 8) / STAGE;
-  static constexpr int SMEM = 1024 + STAGES * STAGE + 1024 + RED_DOUBLES * 8 + BST_DOUBLES * 8;
+  static constexpr int STAGES = (K2TC2_SMEM_KB * 1024 - 2048 - RED_DOUBLES * 8) / STAGE;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 1024 + RED_DOUBLES * 8;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
@@ -172,10 +121,6 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void set_bar(int id) { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
 
 template <int NPAD, int RM>
 __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
@@ -211,7 +156,7 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < NAB; ++a) {
-      mbar_init(&afull[a], CF::ALT ? 4 : CW);
+      mbar_init(&afull[a], CW);
       mbar_init(&aempty[a], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -255,8 +200,7 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
     return;
   }
   K2Part<RMAX> P;
-  if constexpr (CF::BSTG) k2_part_init(P, red, wid >= EPI0 ? wid - EPI0 : 0, CF::NSLOT);
-  else k2_part_init(P, red);
+  k2_part_init(P, red);
   K2Ctx<RMAX> C;
   k2_load_ctx(D, C);
 
@@ -266,17 +210,17 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
       const uint64_t pol_x = D.x_policy == 2 ? policy_evict_last()
                              : (D.x_policy == 1 ? policy_evict_normal() : policy_evict_first());
       const uint64_t pol_b = policy_evict_last();
-      const uint32_t bytes = (uint32_t)(A_BYTES + K2TC2_BATOMS * 4 * D.R * 128);
+      const uint32_t bytes = (uint32_t)(A_BYTES + 4 * 4 * D.R * 128);
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int kb = 0; kb < kblocks; ++kb) {
-          K2_WAIT(&empty[stage], phase ^ 1);
+          mbar_wait(&empty[stage], phase ^ 1);
           if (elect_one()) {
             mbar_expect_tx(&full[stage], bytes);
             tma_load_2d(sA + stage * A_BYTES, &tmX, &full[stage], kb * PK, (int)(t * TILE_M), pol_x);
 #pragma unroll
-            for (int a = 0; a < K2TC2_BATOMS; ++a)
+            for (int a = 0; a < 4; ++a)
               tma_load_2d(sB + stage * CF::B_BYTES + a * CF::B_ATOM, &tmB, &full[stage], kb * KS + a * 128, 0, pol_b);
           }
           __syncwarp();
@@ -286,18 +230,6 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
           }
         }
       }
-      // every load of this pass is issued: pull the first K2TC2_L2PF k-blocks of this CTA's first
-      // tiles of the NEXT pass (X does not change) into L2 while the forward product and the finalize
-      // run (HBM is nearly idle then), so the next pass starts from L2 instead of waiting on HBM
-      if (D.update && elect_one()) {
-        const uint64_t pol_pf = policy_evict_normal();
-        for (int i = 0; i < K2TC2_L2PF; ++i) {
-          const int64_t tt = blockIdx.x + (int64_t)(i / kblocks) * gridDim.x;
-          if (tt >= ntiles) break;
-          tma_prefetch_l2(&tmX, (i % kblocks) * PK, (int)(tt * TILE_M), pol_pf);
-        }
-      }
-      __syncwarp();
     }
   } else if (wid == 1) {
     // ===== MMA issuer: the whole warp walks the pipeline, one elected lane issues =====
@@ -311,16 +243,12 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
         const int acc = lt & 1;
         const uint32_t tph = (lt >> 1) & 1;
-        if constexpr (CF::ACC1) {   // one buffer: wait for the epilogue's read of the previous tile
-          if (lt > 0) K2_WAIT(&tempty[acc ^ 1], ((lt - 1) >> 1) & 1);
-        } else {
-          K2_WAIT(&tempty[acc], tph ^ 1);
-        }
+        mbar_wait(&tempty[acc], tph ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tbase + (uint32_t)(CF::ACC1 ? 0 : acc * CF::ACC_COLS);
+        const uint32_t d_tmem = tbase + (uint32_t)(acc * CF::ACC_COLS);
         for (int kb = 0; kb < kblocks; ++kb) {
-          K2_WAIT(&full[stage], phase);
-          K2_WAIT(&afull[ab], aphase);
+          mbar_wait(&full[stage], phase);
+          mbar_wait(&afull[ab], aphase);
           tc_fence_after();
           const uint32_t a_tmem = tbase + (uint32_t)(A_COL0 + ab * A_COLS);
           const uint64_t bdesc0 = umma_desc_sw128(sB0 + (uint32_t)(stage * CF::B_BYTES));
@@ -330,7 +258,7 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
               const uint32_t dq = CF::SPLITQ ? d_tmem + (uint32_t)((kk >> 2) * NPAD)
                                              : d_tmem + (uint32_t)(((kk >> 2) & 1) * NPAD);
               const bool accum = CF::SPLITQ ? (kb != 0 || (kk & 3) != 0) : (kb != 0 || (kk & 11) != 0);   // first of each group: kk = 0, 4
-              if (!K2TC2_NOMMA) umma_i8_tmem_a(dq, a_tmem + (uint32_t)(8 * kk),
+              umma_i8_tmem_a(dq, a_tmem + (uint32_t)(8 * kk),
                              bdesc0 + (uint64_t)((kk >> 2) * (CF::B_ATOM >> 4) + 2 * (kk & 3)), idesc, accum);
             }
             umma_commit(&empty[stage]);
@@ -361,32 +289,23 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     int stage = 0, ab = 0;
     uint32_t phase = 0, aphase = 0;
-    int seq = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      for (int kb = 0; kb < kblocks; ++kb, ++seq) {
-        // (ALT: a warp also waits for the stages it skips -- TMA completions are not ordered across
-        // stages, and a parity wait must not run more than one phase ahead of its barrier.  aempty
-        // needs no such wait: the MMAs, and so their commits, complete in order)
-        K2_WAIT(&full[stage], phase);
-        if (!CF::ALT || (seq & 1) == h) {
-        K2_WAIT(&aempty[ab], aphase ^ 1);
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        mbar_wait(&aempty[ab], aphase ^ 1);
         tc_fence_after();
-#pragma unroll 1
-        for (int hh = 0; hh < (CF::ALT ? 2 : 1); ++hh) {
-        const int hx = CF::ALT ? hh : h;   // column half of the packed row
-#if !K2TC2_NOCONV
         uint32_t w[NW], w4[CF::SPLITQ ? 1 : NW];
         const uint8_t* row = sA + stage * A_BYTES + c * PK;
 #pragma unroll
         for (int jj = 0; jj < CH; ++jj) {   // logical 16-byte chunk j sits at chunk j ^ (c & 7) (SWIZZLE_128B)
-          const int j = hx * CH + jj;
+          const int j = h * CH + jj;
           const uint4 v = *(const uint4*)(row + ((j ^ (c & 7)) << 4));
           w[4 * jj] = v.x;
           w[4 * jj + 1] = v.y;
           w[4 * jj + 2] = v.z;
           w[4 * jj + 3] = v.w;
         }
-        const uint32_t abase = tmem_base + lane_off + (uint32_t)(A_COL0 + ab * A_COLS + hx * NW);
+        const uint32_t abase = tmem_base + lane_off + (uint32_t)(A_COL0 + ab * A_COLS + h * NW);
         if constexpr (!CF::SPLITQ) {
 #pragma unroll
           for (int u = 0; u < NW; ++u) w4[u] = w[u] >> 4;
@@ -401,15 +320,10 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
           if constexpr (NW == 32) tmem_st32(abase + (uint32_t)(32 * q), o);
           else tmem_st16(abase + (uint32_t)(32 * q), o);
         }
-#endif
-        }
-#if !K2TC2_NOCONV
         tmem_wait_st();
-#endif
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&afull[ab]);
-        }
         if (++stage == CF::STAGES) {
           stage = 0;
           phase ^= 1;
@@ -424,32 +338,13 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
     // ===== epilogue: TMEM lanes 32*(wid%4) .. +31 = columns of the tile =====
     const int q = wid & 3;
     const int eset = (wid - EPI0) >> 2;   // 0, or 0/1 with two epilogue sets (alternate tiles)
-    const int64_t tstep = (int64_t)gridDim.x * CF::ESETS;   // this set's tiles: t0, t0 + tstep, ...
-    // staged beta: this set's tile of beta^k rows is cp.async'ed into bst one set-tile ahead; thread
-    // st copies (and later writes back) elements st, st + 128, ... of the tile's 128 R doubles
-    double* bst = (double*)(smem + CF::STAGES * CF::STAGE + 1024 + CF::RED_DOUBLES * 8) + eset * TILE_M * RMAX;
-    const int st = q * 32 + lane;
-    auto bst_fetch = [&](int64_t tt) {
-      if (tt < ntiles) {
-        const int64_t c0 = tt * TILE_M;
-        const int tot = (int)((D.p - c0 < TILE_M ? D.p - c0 : TILE_M) * C.R);
-        const double* src = C.beta_in + (c0 + 1) * C.R;
-        for (int e = st; e < tot; e += TILE_M) cp_async8(smem_u32(bst + e), src + e);
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    if constexpr (CF::BSTG) bst_fetch(blockIdx.x + (int64_t)eset * gridDim.x);
     int lt = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
       const int acc = lt & 1;
       if (CF::EW == 8 && acc != eset) continue;
       const uint32_t aph = (lt >> 1) & 1;
-      epi_prefetch<RMAX>(D, C, (t + (int64_t)gridDim.x * (CF::EW == 8 ? 2 : 1)) * TILE_M + q * 32 + lane, !CF::BSTG);
-      if (K2TC2_ESLEEP > 0) {
-        while (!mbar_test(&tfull[acc], aph)) __nanosleep(K2TC2_ESLEEP);
-      } else {
-        mbar_wait_park(&tfull[acc], aph);
-      }
+      epi_prefetch<RMAX>(D, C, (t + (int64_t)gridDim.x * (CF::EW == 8 ? 2 : 1)) * TILE_M + q * 32 + lane);
+      mbar_wait_park(&tfull[acc], aph);
       tc_fence_after();
       int32_t dv[NPAD];
       if constexpr (CF::SPLITQ) {
@@ -461,7 +356,7 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
           for (int h = 0; h < NPAD / 16; ++h) {
             uint32_t v[16];
             tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) +
-                          (uint32_t)((CF::ACC1 ? 0 : acc) * CF::ACC_COLS + pq * NPAD + h * 16), v);
+                          (uint32_t)(acc * CF::ACC_COLS + pq * NPAD + h * 16), v);
             tmem_wait_ld();
 #pragma unroll
             for (int u = 0; u < 16; ++u) dv[h * 16 + u] += ((int32_t)v[u]) >> (2 * pq);
@@ -471,8 +366,8 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
 #pragma unroll
         for (int h = 0; h < NPAD / 16; ++h) {
           uint32_t v[16], v1[16];
-          tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((CF::ACC1 ? 0 : acc) * CF::ACC_COLS + h * 16), v);
-          tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((CF::ACC1 ? 0 : acc) * CF::ACC_COLS + NPAD + h * 16), v1);
+          tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * CF::ACC_COLS + h * 16), v);
+          tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * CF::ACC_COLS + NPAD + h * 16), v1);
           tmem_wait_ld();
 #pragma unroll
           for (int u = 0; u < 16; ++u) dv[h * 16 + u] = (int32_t)v[u] + ((int32_t)v1[u] >> 2);
@@ -481,7 +376,6 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (K2TC2_NOEPI) continue;
 
       const int64_t c = t * TILE_M + q * 32 + lane;
       const bool valid = c < D.p;
@@ -496,29 +390,9 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
 #pragma unroll
         for (int r = 0; r < RMAX; ++r) g[r] = 0.0;
       }
-      if constexpr (CF::BSTG) {
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        set_bar(1 + eset);   // the whole tile of beta^k is in bst
-        double* bcol = bst + st * C.R;
-        const bool nz = epi_column<RMAX>(D, C, valid ? c : 0, g, P, valid, bcol, bcol);   // beta^{k+1} in place
-        if (D.update) support_append<RMAX>(D, C, nz, c, bcol);
-        set_bar(1 + eset);   // every column's beta^{k+1} is in bst
-        if (D.update) {      // coalesced write-back of the active RHS, then the set's next tile
-          const int64_t c0 = t * TILE_M;
-          const int tot = (int)((D.p - c0 < TILE_M ? D.p - c0 : TILE_M) * C.R);
-          double* dst = C.beta_out + (c0 + 1) * C.R;
-          for (int e = st; e < tot; e += TILE_M) {
-            const double v = bst[e];
-            if (C.cs->active[e % C.R]) dst[e] = v;
-          }
-        }
-        bst_fetch(t + tstep);   // same elements per thread: its own reads above precede the copies
-      } else {
-        const bool nz = epi_column<RMAX>(D, C, valid ? c : 0, g, P, valid);
-        if (D.update) support_append<RMAX>(D, C, nz, c);
-      }
+      const bool nz = epi_column<RMAX>(D, C, valid ? c : 0, g, P, valid);
+      if (D.update) support_append<RMAX>(D, C, nz, c);
     }
-    if constexpr (CF::BSTG) asm volatile("cp.async.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -526,8 +400,7 @@ __global__ void __launch_bounds__(Cfg2<NPAD, RM>::THREADS, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
   }
-  if constexpr (CF::BSTG) k2_finish<RMAX>(D, C, P, red, CF::NSLOT);
-  else k2_finish<RMAX>(D, C, P, red);
+  k2_finish<RMAX>(D, C, P, red);
 }
 
 // ---------------------------------------------------------------- several RHS: tile-pair order
