@@ -23,6 +23,9 @@
 //   epilogue (warps 8-11): identical to k2_tc.cu.
 // X is read from HBM exactly once per iteration; the CUDA cores spend about two
 // instructions per four samples on unpacking.
+// Two kernels: k2_tc2_kernel (1..4 RHS, one tile at a time) and k2_tc2_pair_kernel (5..16 RHS:
+// two tiles share each theta-digit stage, see its header below); k2p_kernel is the same pipeline
+// for the power / Lanczos back pass of the setup.
 #include <cuda.h>
 
 #include "k2_common.cuh"
